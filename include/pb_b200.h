@@ -1,0 +1,136 @@
+/*
+ * pb_b200.h -- C ABI of the B200-native batched panel-major FP64 engine.
+ *
+ * This is the drop-in boundary for the reference's compute-core surface
+ * (panelblas `_backend` core module, selected in
+ * /root/reference/pkg/src/panelblas/_backend/__init__.py:12-44 and bound
+ * by level3.py:31 / pack.py:15).  Each entry point replaces one core
+ * function, extended with a leading batch dimension:
+ *
+ *   pb_dgemm_nt    <- ccore.gemm_nt_drv   (ccore.pyx:746-771)
+ *   pb_dsyrk_ln    <- ccore.syrk_ln_drv   (ccore.pyx:804-831)
+ *   pb_dtrsm_rltn  <- ccore.trsm_rltn_drv (ccore.pyx:855-874) + the
+ *                     reciprocal selection of level3._recip_diag (level3.py:160-177)
+ *   pb_dpotrf_l    <- ccore.potrf_drv     (ccore.pyx:877-905)
+ *   pb_dpack_cm    <- ccore.kpack_cm      (ccore.pyx:718-723)
+ *   pb_dunpack_cm  <- ccore.kunpack_cm    (ccore.pyx:734-739)
+ *   pb_dgecp       <- ccore.kgecp         (ccore.pyx:677-682)
+ *
+ * Conventions (mirroring the reference core):
+ *   - caller owns every buffer; nothing here allocates device memory;
+ *   - all pointers are DEVICE pointers; work is enqueued on `stream`
+ *     (a cudaStream_t, NULL = legacy default stream) and is asynchronous;
+ *   - panel size ps = 4; element (i, j) of an item lives at
+ *       (i - i%4)*cn + 4*j + i%4      (matstore.py:37-45)
+ *   - windows may start anywhere (ai%4 != 0 included); writes never leave
+ *     the m_store x n_store window (syrk/potrf: lower triangle only);
+ *   - D == C (gemm, syrk, potrf) and D == B (trsm) aliasing is supported;
+ *     partial overlap is undefined (level3.py:14-15);
+ *   - return 0 on success, -i if argument i (1-based) is invalid,
+ *     PB_ERR_CUDA if a launch failed.  Bad pivots are not errors of the
+ *     call: they are reported per item in `info` (-1 = ok, else the first
+ *     failing pivot index, like the core's integer status), so one bad
+ *     item never blocks the others.
+ */
+#ifndef PB_B200_H
+#define PB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_PS 4
+#define PB_ERR_CUDA (-1000)
+
+/* A batch of equally-shaped panel-major matrices: blasfeo_dmat
+ * / panelblas PanelMatrix (matstore.py:68-115) with
+ * a leading batch axis.  Item b's data starts at pA + b*stride and its
+ * diag_inv at dA + b*dA_stride.  stride == 0 broadcasts one matrix to all
+ * items (inputs only). */
+typedef struct pb_dmat_batch {
+  double *pA;        /* panel-major data of item 0                       */
+  double *dA;        /* diag_inv of item 0 (may be NULL if unused)        */
+  int32_t m, n;      /* rows, cols of every item                          */
+  int32_t cn;        /* panel length (blasfeo sda) = round_up(n, 4)       */
+  int32_t batch;     /* number of items                                   */
+  int64_t stride;    /* doubles between consecutive items' pA             */
+  int64_t dA_stride; /* doubles between consecutive items' dA             */
+} pb_dmat_batch;
+
+/* ABI version (bumped on any signature change). */
+int pb_version(void);
+/* Human-readable text of the last error raised on this thread. */
+const char *pb_last_error(void);
+
+/* D = alpha*A*B^T + beta*C (blasfeo_dgemm_nt).
+ * A: m x k at (ai,aj); B: n x k at (bi,bj); C, D: m x n.
+ * alpha == 0 ignores A and B (NaN-safe); beta == 0 never reads C. */
+int pb_dgemm_nt(int m, int n, int k, double alpha,
+                const pb_dmat_batch *sA, int ai, int aj,
+                const pb_dmat_batch *sB, int bi, int bj, double beta,
+                const pb_dmat_batch *sC, int ci, int cj,
+                const pb_dmat_batch *sD, int di, int dj, void *stream);
+
+/* lower(D) = alpha*A*B^T + beta*C, m x m, A and B m x k (blasfeo_dsyrk_ln).
+ * The strict upper triangle of D is never written. */
+int pb_dsyrk_ln(int m, int k, double alpha,
+                const pb_dmat_batch *sA, int ai, int aj,
+                const pb_dmat_batch *sB, int bi, int bj, double beta,
+                const pb_dmat_batch *sC, int ci, int cj,
+                const pb_dmat_batch *sD, int di, int dj, void *stream);
+
+/* D * A^T = alpha*B, A n x n lower non-unit, B and D m x n
+ * (blasfeo_dtrsm_rltn).  Reciprocals of A's diagonal: use_dA != 0 reuses
+ * sA->dA[aj .. aj+n) written by a factorization (level3.py:169-170);
+ * use_dA == 0 computes 1/A[j,j] in-kernel, and an item with a zero
+ * diagonal gets info[b] = j and is left untouched (level3.py:171-177).
+ * info may be NULL when use_dA != 0. */
+int pb_dtrsm_rltn(int m, int n, double alpha,
+                  const pb_dmat_batch *sA, int ai, int aj, int use_dA,
+                  const pb_dmat_batch *sB, int bi, int bj,
+                  const pb_dmat_batch *sD, int di, int dj,
+                  int32_t *info, void *stream);
+
+/* Lower Cholesky factor of lower(C) into D (blasfeo_dpotrf_l), m x n with
+ * n <= m (n < m: trailing rows solved against the factor, the reference's
+ * non-squared variant).  Writes sD->dA[dj .. dj+n) = 1/L[j,j].
+ * info[b] = -1, or the first pivot index with d <= 0 (NaN passes, as in
+ * ccore.pyx:423); a failing item is written exactly as far as the
+ * reference would have written it before returning. */
+int pb_dpotrf_l(int m, int n,
+                const pb_dmat_batch *sC, int ci, int cj,
+                const pb_dmat_batch *sD, int di, int dj,
+                int32_t *info, void *stream);
+
+/* Column-major -> panel-major copy (kpack_cm): item b's source element
+ * (i, j) is S[b*s_stride + i + j*lds]. */
+int pb_dpack_cm(int m, int n, const double *S, int64_t lds, int64_t s_stride,
+                const pb_dmat_batch *sD, int di, int dj, void *stream);
+
+/* Panel-major -> column-major copy (kunpack_cm): Dcm[b*d_stride + i + j*ldd]. */
+int pb_dunpack_cm(int m, int n, const pb_dmat_batch *sS, int si, int sj,
+                  double *Dcm, int64_t ldd, int64_t d_stride, void *stream);
+
+/* Strided variants of pack/unpack for row-major host arrays
+ * (pack.panel_from_array / panel_to_array, pack.py:215-237): element (i, j)
+ * of item b at X[b*x_stride + i*x_row + j*x_col]. */
+int pb_dpack(int m, int n, const double *S, int64_t s_row, int64_t s_col, int64_t s_stride,
+             const pb_dmat_batch *sD, int di, int dj, void *stream);
+int pb_dunpack(int m, int n, const pb_dmat_batch *sS, int si, int sj,
+               double *X, int64_t x_row, int64_t x_col, int64_t x_stride, void *stream);
+
+/* Panel -> panel window copy (kgecp), arbitrary origins on both sides. */
+int pb_dgecp(int m, int n, const pb_dmat_batch *sS, int si, int sj,
+             const pb_dmat_batch *sD, int di, int dj, void *stream);
+
+/* Number of kernels this thread has launched through the ABI since the
+ * last reset (bench.py's gpu_launches evidence). */
+int64_t pb_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PB_B200_H */

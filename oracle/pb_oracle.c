@@ -1,0 +1,280 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- NOT PART OF THE PRODUCT PATH.
+ *
+ * CPU restatement of the reference's hot-path arithmetic (panelblas
+ * `_backend/ccore.pyx`), used by tests/, __graft_entry__.smoke() and the
+ * bench.py cpu_baseline / --impl reference legs as the parity checker.
+ * The product (paper_1704_02457_b200/) never links, loads or calls this.
+ *
+ * Every function works on ONE panel-major item (plain double arrays plus
+ * element offsets, exactly like the reference core) and has a `_batch`
+ * twin that loops over items with explicit item strides.
+ *
+ * Bit-exactness: compiled with -ffp-contract=off (no FMA) and evaluates
+ * each output element with the same operation sequence as the reference
+ * core, so results are bit-identical to the compiled reference (pinned in
+ * tests/test_oracle.py against tests/golden/ and oracle/_ref).
+ *
+ * Why per-element evaluation is the same sequence as the reference's
+ * register-blocked kernels: `_acc_nt` (ccore.pyx:45-127) keeps one
+ * independent accumulator per output element, starts it at 0.0 and adds
+ * A[i,l]*(sign*B[j,l]) for l ascending; the mr=4/8 blocking only changes
+ * which elements share a loop, never the order of one element's sum.
+ */
+#include <math.h>
+#include <stdint.h>
+
+typedef int64_t ix;
+
+/* element_offset: matstore.py:37-45, ccore.pyx:16-18 (ps = 4). */
+static inline ix eo(ix i, ix j, ix sd) { return (i & ~(ix)3) * sd + 4 * j + (i & 3); }
+
+ix po_element_offset(ix i, ix j, ix sd) { return eo(i, j, sd); }
+
+/* memsize_panel_matrix: matstore.py:208-218. */
+static ix ru(ix x, ix to) { return (x + to - 1) / to * to; }
+ix po_memsize(ix m, ix n) {
+  ix mn = m < n ? m : n;
+  return ru(ru(m, 4) * ru(n, 4) * 8, 64) + ru(mn * 8, 64);
+}
+
+/* _store_block scalar rule, ccore.pyx:26-42: alpha==0 ignores acc,
+ * beta==0 never reads C. */
+static inline double store_rule(double alpha, double acc, double beta, const double *c) {
+  if (alpha != 0.0) {
+    double v = alpha * acc;
+    if (beta != 0.0) v += beta * (*c);
+    return v;
+  }
+  if (beta != 0.0) return beta * (*c);
+  return 0.0;
+}
+
+/* _ksyrk_core diagonal-tile rule, ccore.pyx:288-292. */
+static inline double syrk_diag_rule(double alpha, double acc, double beta, const double *c) {
+  double v = (beta != 0.0) ? beta * (*c) : 0.0;
+  if (alpha != 0.0) v = alpha * acc + v;
+  return v;
+}
+
+/* ---- pack / unpack / gecp: ccore.pyx:677-682, 718-723, 734-739 ---- */
+
+void po_pack_cm(ix m, ix n, const double *S, ix so, ix lds, double *D, ix di, ix dj, ix sdd) {
+  for (ix j = 0; j < n; ++j)
+    for (ix i = 0; i < m; ++i) D[eo(di + i, dj + j, sdd)] = S[so + i + j * lds];
+}
+
+void po_unpack_cm(ix m, ix n, const double *S, ix si, ix sj, ix sds, double *D, ix dofs, ix ldd) {
+  for (ix j = 0; j < n; ++j)
+    for (ix i = 0; i < m; ++i) D[dofs + i + j * ldd] = S[eo(si + i, sj + j, sds)];
+}
+
+void po_gecp(ix m, ix n, const double *S, ix si, ix sj, ix sds, double *D, ix di, ix dj, ix sdd) {
+  for (ix j = 0; j < n; ++j)
+    for (ix i = 0; i < m; ++i) D[eo(di + i, dj + j, sdd)] = S[eo(si + i, sj + j, sds)];
+}
+
+/* ---- gemm_nt: level3.py:81-98 + gemm_nt_drv ccore.pyx:746-771 ----
+ * D = alpha*A*B^T + beta*C.  Unaligned stream windows are read in place
+ * (the reference's _aligned_stream repack is a bit-exact copy). */
+void po_gemm_nt(ix m, ix n, ix k, double alpha,
+                const double *A, ix ai, ix aj, ix sda,
+                const double *B, ix bi, ix bj, ix sdb, double beta,
+                const double *C, ix ci, ix cj, ix sdc,
+                double *D, ix di, ix dj, ix sdd) {
+  for (ix j = 0; j < n; ++j)
+    for (ix i = 0; i < m; ++i) {
+      double s = 0.0;
+      for (ix l = 0; l < k; ++l) s += A[eo(ai + i, aj + l, sda)] * B[eo(bi + j, bj + l, sdb)];
+      D[eo(di + i, dj + j, sdd)] = store_rule(alpha, s, beta, &C[eo(ci + i, cj + j, sdc)]);
+    }
+}
+
+/* ---- syrk_ln: level3.py:120-137 + syrk_ln_drv ccore.pyx:804-831 ----
+ * Lower triangle only; elements inside a diagonal 4x4 tile use the
+ * _ksyrk_core rule, the rest the _store_block rule. */
+void po_syrk_ln(ix m, ix k, double alpha,
+                const double *A, ix ai, ix aj, ix sda,
+                const double *B, ix bi, ix bj, ix sdb, double beta,
+                const double *C, ix ci, ix cj, ix sdc,
+                double *D, ix di, ix dj, ix sdd) {
+  for (ix j = 0; j < m; ++j)
+    for (ix i = j; i < m; ++i) {
+      double s = 0.0;
+      for (ix l = 0; l < k; ++l) s += A[eo(ai + i, aj + l, sda)] * B[eo(bi + j, bj + l, sdb)];
+      const double *c = &C[eo(ci + i, cj + j, sdc)];
+      D[eo(di + i, dj + j, sdd)] =
+          ((i >> 2) == (j >> 2)) ? syrk_diag_rule(alpha, s, beta, c) : store_rule(alpha, s, beta, c);
+    }
+}
+
+/* One 4-wide column block of a right-transposed lower solve, shared by
+ * trsm_rltn and the off-diagonal tiles of potrf (_trsm_rltn_core,
+ * ccore.pyx:358-388 with kp = 0):
+ *   acc = -sum_{l<jj} X[r,l]*T[jj+c,l]   (l ascending, from 0.0)
+ *   acc += alpha*Bv[r,c]
+ *   acc -= X[r,jj+t]*T[jj+c,jj+t]        (t < c ascending, solved values)
+ *   acc *= dinv[jj+c]                     (unless unit)
+ * X is the output (already-solved columns), T the triangular factor.
+ * Stores column by column into X, like the reference. */
+static void rltn_block(ix rows, ix jj, ix ns, double alpha,
+                       const double *T, ix ti, ix tj, ix sdt, int unit,
+                       const double *Bv, ix bi, ix bj, ix sdb,
+                       double *X, ix xi, ix xj, ix sdx,
+                       const double *dinv, ix dio) {
+  /* all downdates first, then the reference's column-outer loop, so that
+   * in-place X == Bv reads B before the column is overwritten */
+  double acc[4][4];
+  for (ix r = 0; r < rows; ++r)
+    for (ix c = 0; c < ns; ++c) {
+      double s = 0.0;
+      for (ix l = 0; l < jj; ++l) s += X[eo(xi + r, xj + l, sdx)] * (-T[eo(ti + jj + c, tj + l, sdt)]);
+      acc[c][r] = s;
+    }
+  for (ix c = 0; c < ns; ++c) {
+    for (ix r = 0; r < rows; ++r) acc[c][r] += alpha * Bv[eo(bi + r, bj + jj + c, sdb)];
+    for (ix t = 0; t < c; ++t) {
+      double e = T[eo(ti + jj + c, tj + jj + t, sdt)];
+      for (ix r = 0; r < rows; ++r) acc[c][r] -= acc[t][r] * e;
+    }
+    if (!unit) {
+      double inv = dinv[dio + jj + c];
+      for (ix r = 0; r < rows; ++r) acc[c][r] *= inv;
+    }
+    for (ix r = 0; r < rows; ++r) X[eo(xi + r, xj + jj + c, sdx)] = acc[c][r];
+  }
+}
+
+/* ---- trsm_rltn: trsm_rltn_drv ccore.pyx:855-874 ----
+ * D*A^T = alpha*B, A lower (non-unit unless `unit`); reciprocals come from
+ * dinv[dio + j] (level3.py:160-177 decides where they come from). */
+void po_trsm_rltn(ix m, ix n, double alpha,
+                  const double *A, ix ai, ix aj, ix sda, int unit,
+                  const double *B, ix bi, ix bj, ix sdb,
+                  double *D, ix di, ix dj, ix sdd,
+                  const double *dinv, ix dio) {
+  for (ix ii = 0; ii < m; ii += 4) {
+    ix ms = m - ii < 4 ? m - ii : 4;
+    for (ix jj = 0; jj < n; jj += 4) {
+      ix ns = n - jj < 4 ? n - jj : 4;
+      rltn_block(ms, jj, ns, alpha, A, ai, aj, sda, unit, B, bi + ii, bj, sdb, D, di + ii, dj, sdd, dinv, dio);
+    }
+  }
+}
+
+/* ---- potrf_l: potrf_drv ccore.pyx:877-905, _kpotrf_core :404-438 ----
+ * Block-row ("up-looking") order; returns -1 or the first failing pivot
+ * index.  On failure the failing diagonal tile is not stored, earlier
+ * tiles and dinv[dio .. dio+index) are, exactly like the reference.
+ * n < m: the trailing m-n rows are solved against the factor (tall). */
+int po_potrf_l(ix m, ix n, const double *C, ix ci, ix cj, ix sdc,
+               double *D, ix di, ix dj, ix sdd, double *dinv, ix dio) {
+  for (ix ii = 0; ii < m; ii += 4) {
+    ix ms = m - ii < 4 ? m - ii : 4;
+    ix jmax = ii + 4 < n ? ii + 4 : n;
+    for (ix jj = 0; jj < jmax; jj += 4) {
+      ix ns = n - jj < 4 ? n - jj : 4;
+      if (jj < ii) {
+        rltn_block(ms, jj, ns, 1.0, D, di, dj, sdd, 0, C, ci + ii, cj, sdc, D, di + ii, dj, sdd, dinv, dio);
+        continue;
+      }
+      /* diagonal tile: downdate, add C, in-register right-looking factor */
+      double acc[4][4];
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = 0; r < ms; ++r) {
+          double s = 0.0;
+          for (ix l = 0; l < jj; ++l)
+            s += D[eo(di + ii + r, dj + l, sdd)] * (-D[eo(di + jj + c, dj + l, sdd)]);
+          acc[c][r] = s;
+        }
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = 0; r < ms; ++r) acc[c][r] += C[eo(ci + ii + r, cj + jj + c, sdc)];
+      for (ix c = 0; c < ns; ++c) {
+        double d = acc[c][c];
+        if (d <= 0.0) return (int)(jj + c); /* NaN passes, as in the reference */
+        double ljj = sqrt(d);
+        double inv = 1.0 / ljj;
+        acc[c][c] = ljj;
+        dinv[dio + jj + c] = inv;
+        for (ix r = c + 1; r < ms; ++r) acc[c][r] *= inv;
+        for (ix c2 = c + 1; c2 < ns; ++c2) {
+          double lcj = acc[c][c2];
+          for (ix r = c2; r < ms; ++r) acc[c2][r] -= acc[c][r] * lcj;
+        }
+      }
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = c; r < ms; ++r) D[eo(di + ii + r, dj + jj + c, sdd)] = acc[c][r];
+    }
+  }
+  return -1;
+}
+
+/* ---- naive column-major oracles: ccore.pyx:1109-1223 (o_*) ----
+ * Independent of the panel machinery; used to cross-check the above. */
+void po_naive_potrf(ix m, const double *C, ix ldc, double *L, ix ldl) {
+  for (ix j = 0; j < m; ++j) {
+    double s = C[j + j * ldc];
+    for (ix t = 0; t < j; ++t) s -= L[j + t * ldl] * L[j + t * ldl];
+    double ljj = sqrt(s);
+    L[j + j * ldl] = ljj;
+    for (ix i = j + 1; i < m; ++i) {
+      double v = C[i + j * ldc];
+      for (ix t = 0; t < j; ++t) v -= L[i + t * ldl] * L[j + t * ldl];
+      L[i + j * ldl] = v / ljj;
+    }
+  }
+}
+
+/* ---- batch loops (item strides in doubles; stride 0 broadcasts) ---- */
+
+void po_pack_cm_batch(ix nb, ix m, ix n, const double *S, ix lds, ix s_stride,
+                      double *D, ix di, ix dj, ix sdd, ix d_stride) {
+  for (ix b = 0; b < nb; ++b) po_pack_cm(m, n, S + b * s_stride, 0, lds, D + b * d_stride, di, dj, sdd);
+}
+
+void po_unpack_cm_batch(ix nb, ix m, ix n, const double *S, ix si, ix sj, ix sds, ix s_stride,
+                        double *D, ix ldd, ix d_stride) {
+  for (ix b = 0; b < nb; ++b) po_unpack_cm(m, n, S + b * s_stride, si, sj, sds, D + b * d_stride, 0, ldd);
+}
+
+void po_gecp_batch(ix nb, ix m, ix n, const double *S, ix si, ix sj, ix sds, ix s_stride,
+                   double *D, ix di, ix dj, ix sdd, ix d_stride) {
+  for (ix b = 0; b < nb; ++b) po_gecp(m, n, S + b * s_stride, si, sj, sds, D + b * d_stride, di, dj, sdd);
+}
+
+void po_gemm_nt_batch(ix nb, ix m, ix n, ix k, double alpha,
+                      const double *A, ix ai, ix aj, ix sda, ix as,
+                      const double *B, ix bi, ix bj, ix sdb, ix bs, double beta,
+                      const double *C, ix ci, ix cj, ix sdc, ix cs,
+                      double *D, ix di, ix dj, ix sdd, ix ds) {
+  for (ix b = 0; b < nb; ++b)
+    po_gemm_nt(m, n, k, alpha, A + b * as, ai, aj, sda, B + b * bs, bi, bj, sdb, beta,
+               C + b * cs, ci, cj, sdc, D + b * ds, di, dj, sdd);
+}
+
+void po_syrk_ln_batch(ix nb, ix m, ix k, double alpha,
+                      const double *A, ix ai, ix aj, ix sda, ix as,
+                      const double *B, ix bi, ix bj, ix sdb, ix bs, double beta,
+                      const double *C, ix ci, ix cj, ix sdc, ix cs,
+                      double *D, ix di, ix dj, ix sdd, ix ds) {
+  for (ix b = 0; b < nb; ++b)
+    po_syrk_ln(m, k, alpha, A + b * as, ai, aj, sda, B + b * bs, bi, bj, sdb, beta,
+               C + b * cs, ci, cj, sdc, D + b * ds, di, dj, sdd);
+}
+
+void po_trsm_rltn_batch(ix nb, ix m, ix n, double alpha,
+                        const double *A, ix ai, ix aj, ix sda, ix as, int unit,
+                        const double *B, ix bi, ix bj, ix sdb, ix bs,
+                        double *D, ix di, ix dj, ix sdd, ix ds,
+                        const double *dinv, ix dio, ix dinv_stride) {
+  for (ix b = 0; b < nb; ++b)
+    po_trsm_rltn(m, n, alpha, A + b * as, ai, aj, sda, unit, B + b * bs, bi, bj, sdb,
+                 D + b * ds, di, dj, sdd, dinv + b * dinv_stride, dio);
+}
+
+void po_potrf_l_batch(ix nb, ix m, ix n, const double *C, ix ci, ix cj, ix sdc, ix cs,
+                      double *D, ix di, ix dj, ix sdd, ix ds, double *dinv, ix dio, ix dinv_stride,
+                      int32_t *info) {
+  for (ix b = 0; b < nb; ++b)
+    info[b] = po_potrf_l(m, n, C + b * cs, ci, cj, sdc, D + b * ds, di, dj, sdd, dinv + b * dinv_stride, dio);
+}

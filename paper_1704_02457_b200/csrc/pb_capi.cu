@@ -1,0 +1,318 @@
+// extern "C" entry points of libpb_b200.so (declared in include/pb_b200.h).
+//
+// Validation mirrors the reference's L3 checks (level3.py:47-53,
+// pack.py:36-42): negative sizes and windows leaving the matrix are
+// rejected before anything is launched (return -argument_position); the
+// Python layer turns those into DimensionError with the reference's text.
+// Sizes that do not fit one CTA's shared memory are handled by a blocked
+// driver built from the same kernels (potrf: tall panel factor + syrk
+// downdate + recursive trailing factor; trsm: column-block solve + gemm
+// downdate), so every size the reference accepts runs on the GPU.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+static thread_local std::string t_err;
+static thread_local int64_t t_launches = 0;
+void note_launch() { ++t_launches; }
+
+static int fail_arg(int pos, const char *what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "argument %d: %s", pos, what);
+  t_err = buf;
+  return -pos;
+}
+
+static int cuda_fail(cudaError_t e) {
+  t_err = std::string("CUDA: ") + cudaGetErrorString(e);
+  return PB_ERR_CUDA;
+}
+
+static Mat to_mat(const pb_dmat_batch *x) {
+  Mat r;
+  r.p = x->pA;
+  r.stride = x->stride;
+  r.cn = x->cn;
+  r.d = x->dA;
+  r.dstride = x->dA_stride;
+  return r;
+}
+
+// Check one operand: descriptor sanity and window (i0, j0, rows, cols).
+static int check_mat(const pb_dmat_batch *x, int pos_mat, int i0, int j0, int64_t rows, int64_t cols, int batch,
+                     bool is_output) {
+  if (!x) return fail_arg(pos_mat, "null matrix descriptor");
+  if (x->m < 0 || x->n < 0) return fail_arg(pos_mat, "negative matrix size");
+  if (x->cn < ((x->n + 3) & ~3) || (x->cn & 3)) return fail_arg(pos_mat, "panel length must be round_up(n,4)");
+  if (i0 < 0 || j0 < 0) return fail_arg(pos_mat + 1, "negative sub-matrix origin");
+  if (i0 + rows > x->m || j0 + cols > x->n) return fail_arg(pos_mat, "window exceeds matrix");
+  if (rows > 0 && cols > 0 && !x->pA) return fail_arg(pos_mat, "null data pointer");
+  if (is_output) {
+    if (x->stride <= 0 && batch > 1) return fail_arg(pos_mat, "output needs a positive item stride");
+  } else if (x->stride != 0 && x->batch != batch) {
+    return fail_arg(pos_mat, "batch size differs from the output's");
+  }
+  if (x->stride < 0) return fail_arg(pos_mat, "negative item stride");
+  return 0;
+}
+
+static bool vec16_ok(const pb_dmat_batch *x, int i0) {
+  return (i0 & 3) == 0 && ((uintptr_t)x->pA & 15) == 0 && (x->stride & 1) == 0;
+}
+
+static int finish(cudaError_t e) { return e == cudaSuccess ? 0 : cuda_fail(e); }
+
+}  // namespace pb
+
+using namespace pb;
+
+extern "C" {
+
+int pb_version(void) { return 1; }
+const char *pb_last_error(void) { return t_err.c_str(); }
+int64_t pb_launch_count(int reset) {
+  const int64_t v = t_launches;
+  if (reset) t_launches = 0;
+  return v;
+}
+
+static int gemm_common(bool syrk, int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj,
+                       const pb_dmat_batch *sB, int bi, int bj, double beta, const pb_dmat_batch *sC, int ci,
+                       int cj, const pb_dmat_batch *sD, int di, int dj, void *stream, const int32_t *skip) {
+  // positions: gemm (m1 n2 k3 alpha4 A5 ai6 aj7 B8 bi9 bj10 beta11 C12 ci13 cj14 D15 di16 dj17)
+  //            syrk (m1 k2 alpha3 A4 ai5 aj6 B7 bi8 bj9 beta10 C11 ci12 cj13 D14 di15 dj16)
+  const int o = syrk ? -1 : 0;
+  if (m < 0) return fail_arg(1, "negative size");
+  if (!syrk && n < 0) return fail_arg(2, "negative size");
+  if (k < 0) return fail_arg(3 + o, "negative size");
+  if (!sD) return fail_arg(15 + o, "null matrix descriptor");
+  const int batch = sD->batch;
+  if (batch < 0) return fail_arg(15 + o, "negative batch");
+  const int64_t nn = syrk ? m : n;
+  int r;
+  if ((r = check_mat(sA, 5 + o, ai, aj, m, k, batch, false))) return r;
+  if ((r = check_mat(sB, 8 + o, bi, bj, nn, k, batch, false))) return r;
+  if ((r = check_mat(sC, 12 + o, ci, cj, m, nn, batch, false))) return r;
+  if ((r = check_mat(sD, 15 + o, di, dj, m, nn, batch, true))) return r;
+  if (m == 0 || nn == 0 || batch == 0) return 0;  // level3.py:91-92, 130-131
+  GemmArgs g;
+  g.m = m;
+  g.n = nn;
+  g.k = k;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.A = to_mat(sA);
+  g.B = to_mat(sB);
+  g.C = to_mat(sC);
+  g.D = to_mat(sD);
+  g.ai = ai, g.aj = aj, g.bi = bi, g.bj = bj, g.ci = ci, g.cj = cj, g.di = di, g.dj = dj;
+  g.batch = batch;
+  g.vecA = vec16_ok(sA, ai);
+  g.vecB = vec16_ok(sB, bi);
+  g.skip = skip;
+  cudaStream_t st = (cudaStream_t)stream;
+  return finish(syrk ? run_syrk_ln(g, st) : run_gemm_nt(g, st));
+}
+
+int pb_dgemm_nt(int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
+                int bi, int bj, double beta, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
+                int dj, void *stream) {
+  return gemm_common(false, m, n, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+}
+
+int pb_dsyrk_ln(int m, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                int bj, double beta, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+                void *stream) {
+  return gemm_common(true, m, 0, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+}
+
+// ---- trsm_rltn ----------------------------------------------------------
+
+static int trsm_run(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, int aj, int use_dA,
+                    const pb_dmat_batch *sB, int bi, int bj, const pb_dmat_batch *sD, int di, int dj, int32_t *info,
+                    const int32_t *skip, cudaStream_t st) {
+  if (trsm_fits(m, n)) {
+    TrsmArgs g;
+    g.m = m, g.n = n, g.alpha = alpha;
+    g.A = to_mat(sA), g.B = to_mat(sB), g.D = to_mat(sD);
+    g.ai = ai, g.aj = aj, g.bi = bi, g.bj = bj, g.di = di, g.dj = dj;
+    g.use_dA = use_dA;
+    g.info = info;
+    g.batch = sD->batch;
+    g.skip = skip;
+    return finish(run_trsm_rltn(g, st));
+  }
+  // blocked: D1 = solve(B1, A11); D2 = alpha*B2 - D1*A21^T; D2 = solve(D2, A22)
+  int n1 = 8;
+  while (n1 + 8 < n && trsm_fits(m, n1 + 8)) n1 += 8;
+  int r;
+  if ((r = trsm_run(m, n1, alpha, sA, ai, aj, use_dA, sB, bi, bj, sD, di, dj, nullptr, skip, st))) return r;
+  GemmArgs g;
+  g.m = m, g.n = n - n1, g.k = n1, g.alpha = -1.0, g.beta = alpha;
+  g.A = to_mat(sD), g.B = to_mat(sA), g.C = to_mat(sB), g.D = to_mat(sD);
+  g.ai = di, g.aj = dj, g.bi = ai + n1, g.bj = aj, g.ci = bi, g.cj = bj + n1, g.di = di, g.dj = dj + n1;
+  g.batch = sD->batch;
+  g.vecA = vec16_ok(sD, di);
+  g.vecB = vec16_ok(sA, ai + n1);
+  g.skip = skip;
+  if ((r = finish(run_gemm_nt(g, st)))) return r;
+  return trsm_run(m, n - n1, 1.0, sA, ai + n1, aj + n1, use_dA, sD, di, dj + n1, sD, di, dj + n1, nullptr, skip, st);
+}
+
+int pb_dtrsm_rltn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, int aj, int use_dA,
+                  const pb_dmat_batch *sB, int bi, int bj, const pb_dmat_batch *sD, int di, int dj, int32_t *info,
+                  void *stream) {
+  // positions: m1 n2 alpha3 A4 ai5 aj6 use_dA7 B8 bi9 bj10 D11 di12 dj13 info14
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sD) return fail_arg(11, "null matrix descriptor");
+  const int batch = sD->batch;
+  int r;
+  if ((r = check_mat(sA, 4, ai, aj, n, n, batch, false))) return r;
+  if ((r = check_mat(sB, 8, bi, bj, m, n, batch, false))) return r;
+  if ((r = check_mat(sD, 11, di, dj, m, n, batch, true))) return r;
+  if (use_dA && n > 0 && !sA->dA) return fail_arg(4, "use_dA set but the factor has no diag_inv");
+  if (!use_dA && !info) return fail_arg(14, "info is required when reciprocals are computed");
+  if (m == 0 || n == 0 || batch == 0) return 0;  // level3.py:200-201
+  cudaStream_t st = (cudaStream_t)stream;
+  if (trsm_fits(m, n)) return trsm_run(m, n, alpha, sA, ai, aj, use_dA, sB, bi, bj, sD, di, dj, info, nullptr, st);
+  // blocked path: the zero-pivot check covers the whole diagonal first, so a
+  // singular item is left completely untouched (level3.py:171-177)
+  if (info) {
+    if (!use_dA) {
+      if ((r = finish(run_diag_check(to_mat(sA), ai, aj, n, batch, info, st)))) return r;
+    } else if ((r = finish(cudaMemsetAsync(info, 0xff, sizeof(int32_t) * batch, st)))) {
+      return r;
+    }
+  }
+  return trsm_run(m, n, alpha, sA, ai, aj, use_dA, sB, bi, bj, sD, di, dj, nullptr, info, st);
+}
+
+// ---- potrf_l ------------------------------------------------------------
+
+static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+                     int32_t *info, int merge, int off, cudaStream_t st) {
+  if (potrf_fits(m, n)) {
+    PotrfArgs g;
+    g.m = m, g.n = n;
+    g.C = to_mat(sC), g.D = to_mat(sD);
+    g.ci = ci, g.cj = cj, g.di = di, g.dj = dj;
+    g.info = info;
+    g.batch = sD->batch;
+    g.merge = merge;
+    g.info_offset = off;
+    return finish(run_potrf_l(g, st));
+  }
+  // blocked: tall panel factor of the first n1 columns, syrk downdate of
+  // the trailing block, recursive factor of the trailing block.
+  int n1 = 8;
+  while (n1 + 8 < n && potrf_fits(m, n1 + 8)) n1 += 8;
+  int r;
+  if ((r = potrf_run(m, n1, sC, ci, cj, sD, di, dj, info, merge, off, st))) return r;
+  GemmArgs g;
+  g.m = m - n1, g.n = m - n1, g.k = n1, g.alpha = -1.0, g.beta = 1.0;
+  g.A = to_mat(sD), g.B = to_mat(sD), g.C = to_mat(sC), g.D = to_mat(sD);
+  g.ai = di + n1, g.aj = dj, g.bi = di + n1, g.bj = dj, g.ci = ci + n1, g.cj = cj + n1, g.di = di + n1,
+  g.dj = dj + n1;
+  g.batch = sD->batch;
+  g.vecA = g.vecB = vec16_ok(sD, di + n1);
+  g.skip = info;
+  if ((r = finish(run_syrk_ln(g, st)))) return r;
+  return potrf_run(m - n1, n - n1, sD, di + n1, dj + n1, sD, di + n1, dj + n1, info, 1, off + n1, st);
+}
+
+int pb_dpotrf_l(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+                int32_t *info, void *stream) {
+  // positions: m1 n2 C3 ci4 cj5 D6 di7 dj8 info9
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0 || n > m) return fail_arg(2, "potrf_l needs 0 <= n <= m");
+  if (!sD) return fail_arg(6, "null matrix descriptor");
+  const int batch = sD->batch;
+  int r;
+  if ((r = check_mat(sC, 3, ci, cj, m, n, batch, false))) return r;
+  if ((r = check_mat(sD, 6, di, dj, m, n, batch, true))) return r;
+  if (n == 0 || batch == 0) return 0;  // level3.py:335-336
+  if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
+  if (!info) return fail_arg(9, "info is required");
+  return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, (cudaStream_t)stream);
+}
+
+// ---- pack / unpack / gecp ------------------------------------------------
+
+int pb_dpack(int m, int n, const double *S, int64_t s_row, int64_t s_col, int64_t s_stride, const pb_dmat_batch *sD,
+             int di, int dj, void *stream) {
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sD) return fail_arg(7, "null matrix descriptor");
+  int r;
+  if ((r = check_mat(sD, 7, di, dj, m, n, sD->batch, true))) return r;
+  if (m == 0 || n == 0 || sD->batch == 0) return 0;
+  if (!S) return fail_arg(3, "null source");
+  CopyArgs g;
+  memset(&g, 0, sizeof g);
+  g.m = m, g.n = n;
+  g.X = S;
+  g.x_row = s_row, g.x_col = s_col, g.x_stride = s_stride;
+  g.D = to_mat(sD);
+  g.di = di, g.dj = dj;
+  g.batch = sD->batch;
+  return finish(run_pack(g, (cudaStream_t)stream));
+}
+
+int pb_dpack_cm(int m, int n, const double *S, int64_t lds, int64_t s_stride, const pb_dmat_batch *sD, int di, int dj,
+                void *stream) {
+  if (lds < (m > 1 ? m : 1)) return fail_arg(4, "lds < rows");
+  const int r = pb_dpack(m, n, S, 1, lds, s_stride, sD, di, dj, stream);
+  return r == -7 ? -6 : r;
+}
+
+int pb_dunpack(int m, int n, const pb_dmat_batch *sS, int si, int sj, double *X, int64_t x_row, int64_t x_col,
+               int64_t x_stride, void *stream) {
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sS) return fail_arg(3, "null matrix descriptor");
+  int r;
+  if ((r = check_mat(sS, 3, si, sj, m, n, sS->batch, false))) return r;
+  if (m == 0 || n == 0 || sS->batch == 0) return 0;
+  if (!X) return fail_arg(6, "null destination");
+  CopyArgs g;
+  memset(&g, 0, sizeof g);
+  g.m = m, g.n = n;
+  g.Xw = X;
+  g.x_row = x_row, g.x_col = x_col, g.x_stride = x_stride;
+  g.S = to_mat(sS);
+  g.si = si, g.sj = sj;
+  g.batch = sS->batch;
+  return finish(run_unpack(g, (cudaStream_t)stream));
+}
+
+int pb_dunpack_cm(int m, int n, const pb_dmat_batch *sS, int si, int sj, double *Dcm, int64_t ldd, int64_t d_stride,
+                  void *stream) {
+  if (ldd < (m > 1 ? m : 1)) return fail_arg(7, "ldd < rows");
+  return pb_dunpack(m, n, sS, si, sj, Dcm, 1, ldd, d_stride, stream);
+}
+
+int pb_dgecp(int m, int n, const pb_dmat_batch *sS, int si, int sj, const pb_dmat_batch *sD, int di, int dj,
+             void *stream) {
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sD) return fail_arg(6, "null matrix descriptor");
+  int r;
+  if ((r = check_mat(sS, 3, si, sj, m, n, sD->batch, false))) return r;
+  if ((r = check_mat(sD, 6, di, dj, m, n, sD->batch, true))) return r;
+  if (m == 0 || n == 0 || sD->batch == 0) return 0;
+  CopyArgs g;
+  memset(&g, 0, sizeof g);
+  g.m = m, g.n = n;
+  g.S = to_mat(sS);
+  g.D = to_mat(sD);
+  g.si = si, g.sj = sj, g.di = di, g.dj = dj;
+  g.batch = sD->batch;
+  return finish(run_gecp(g, (cudaStream_t)stream));
+}
+
+}  // extern "C"

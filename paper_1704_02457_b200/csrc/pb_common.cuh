@@ -1,0 +1,64 @@
+// Shared device helpers for the panel-major FP64 kernels (sm_100a).
+//
+// Panel-major addressing (ps = 4, matstore.py:37-45): element (i, j) of a
+// matrix with panel length cn lives at (i & ~3)*cn + 4*j + (i & 3).  An
+// 8-row x 4-column block at a panel-aligned row is therefore two
+// contiguous 128-byte runs, which is exactly one m8n8k4 f64 A (or B)
+// fragment: lane t holds element (row t>>2, col t&3) and lanes 0-15 /
+// 16-31 each read one 128-byte run -> conflict-free in shared memory and
+// fully coalesced in global memory.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pb_b200.h"
+
+namespace pb {
+
+typedef int64_t ix;
+
+__host__ __device__ __forceinline__ ix eo(ix i, ix j, ix cn) { return (i & ~(ix)3) * cn + 4 * j + (i & 3); }
+
+// Per-launch view of one operand: item base pointer + stride + panel length.
+struct Mat {
+  double *p;
+  ix stride;  // doubles between items (0 = broadcast)
+  ix cn;      // panel length
+  double *d;  // diag_inv of item 0
+  ix dstride;
+  __device__ __forceinline__ double *item(ix b) const { return p + b * stride; }
+  __device__ __forceinline__ double *ditem(ix b) const { return d + b * dstride; }
+};
+
+// m8n8k4 f64 MMA, D = A*B + C (SASS: DMMA.8x8x4).
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// cp.async helpers (LDGSTS).  src_bytes < size zero-fills the remainder.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ double ldg_nc(const double *p) { return __ldg(p); }
+
+// Named barrier for a team of `nthreads` (multiple of 32) with id 1..15.
+__device__ __forceinline__ void team_sync(int id, int nthreads) {
+  if (nthreads == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+  }
+}
+
+}  // namespace pb

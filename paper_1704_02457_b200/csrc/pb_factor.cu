@@ -1,0 +1,408 @@
+// Batched dpotrf_l and dtrsm_rltn on panel-major FP64 storage (sm_100a).
+//
+// Reference semantics: potrf_drv ccore.pyx:877-905 (+ _kpotrf_core
+// :404-438, _trsm_rltn_core :358-388), trsm_rltn_drv ccore.pyx:855-874,
+// reciprocal selection level3._recip_diag level3.py:160-177.
+//
+// Design (B200-first, not the reference's 4x4 CPU blocking):
+//  * a "team" of TW warps owns one item at a time; the item's lower
+//    trapezoid lives in shared memory in a compact tri-panel layout (panel
+//    pair g holds only columns [0, 8g+8)), so n <= 232 fits one CTA;
+//  * left-looking over 8-column blocks: every 8x8 output tile is one
+//    m8n8k4 accumulator; the downdate  tile -= L[g,:j] L[j,:j]^T  runs on
+//    DMMA straight from shared memory (fragments = two 128-byte runs);
+//  * the 8x8 diagonal factor and the 8-column triangular solves run in
+//    registers with warp shuffles (sqrt and one reciprocal per column, then
+//    multiplies, like the reference's dinv convention ccore.pyx:426-428);
+//  * several teams per CTA, and many CTAs per SM for small n, hide the
+//    serial sqrt/reciprocal chain.
+// Bad pivots: the first index with d <= 0 (NaN passes, ccore.pyx:423) goes
+// to info[b]; the write-back then stores exactly the part of D the
+// reference would have stored before returning, and dinv[0, index).
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+// ---- compact tri-panel layout ---------------------------------------------
+// Row group g (rows 8g..8g+7, panels 2g and 2g+1) stores columns
+// [0, w_g), w_g = min(8g+8, cn8), cn8 = round_up(n, 8).
+struct Tri {
+  int gn;   // column groups = cn8 / 8
+  int cn8;
+  __device__ __forceinline__ int width(int g) const { return g < gn ? 8 * g + 8 : cn8; }
+  __device__ __forceinline__ int group_off(int g) const {
+    return g < gn ? 32 * g * (g + 1) : 32 * gn * (gn + 1) + 8 * (g - gn) * cn8;
+  }
+  // element (r, c) with c < width(r/8)
+  __device__ __forceinline__ int off(int r, int c) const {
+    const int g = r >> 3;
+    return group_off(g) + ((r >> 2) & 1) * 4 * width(g) + 4 * c + (r & 3);
+  }
+  static __host__ __device__ ix size(ix m, ix n) {
+    const ix cn8 = (n + 7) / 8 * 8, gn = cn8 / 8, gm = (m + 7) / 8;
+    return gm <= gn ? 32 * gm * (gm + 1) : 32 * gn * (gn + 1) + 8 * (gm - gn) * cn8;
+  }
+};
+
+// Fragment offset of (row group g, k-step kk) for lane: rows 8g+(lane>>2),
+// col 4kk+(lane&3).
+__device__ __forceinline__ int tri_frag(const Tri &t, int g, int kk, int lane) {
+  return t.group_off(g) + (lane >> 4) * 4 * t.width(g) + 16 * kk + 4 * (lane & 3) + ((lane >> 2) & 3);
+}
+
+// In-register solve of an 8x8 accumulator tile x (fragment layout: lane
+// holds row lane>>2, cols 2(lane&3)+e) against the lower 8x8 diagonal
+// block L (shared, tri layout at rows/cols 8j..), x <- x * L^{-T}, with
+// reciprocals dinv (shared).  ncol = valid columns in the block.
+__device__ __forceinline__ void solve_tile_rt(double (&x)[2], const double *S, const Tri &t, int j,
+                                              const double *dinv, int ncol, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < ncol) {
+      const double inv = dinv[8 * j + c];
+      if (fc == (c >> 1)) x[c & 1] = __dmul_rn(x[c & 1], inv);
+      const double xc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c2 = 2 * fc + e;
+        if (c2 > c && c2 < ncol) x[e] = fma(-xc, S[t.off(8 * j + c2, 8 * j + c)], x[e]);
+      }
+    }
+  }
+}
+
+// Right-looking in-register Cholesky of the 8x8 diagonal tile (fragment
+// layout).  Returns the first failing column (d <= 0) or -1.  On return the
+// tile holds L for columns < the failing one; dinv_out[c] = 1/L[c,c].
+__device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double *dinv_out, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  int fail = -1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < ncol && fail < 0) {
+      const double d = __shfl_sync(0xffffffffu, x[c & 1], c * 4 + (c >> 1));
+      if (d <= 0.0) {
+        fail = c;
+      } else {
+        const double ljj = sqrt(d);
+        const double inv = 1.0 / ljj;
+        if (fc == (c >> 1)) {
+          if (fr == c) x[c & 1] = ljj;
+          else if (fr > c) x[c & 1] = __dmul_rn(x[c & 1], inv);
+        }
+        if (lane == 0) dinv_out[c] = inv;
+        const double lrc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
+        const double l0 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc) * 4 + (c >> 1));
+        const double l1 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc + 1) * 4 + (c >> 1));
+        if (2 * fc > c) x[0] = fma(-lrc, l0, x[0]);
+        if (2 * fc + 1 > c) x[1] = fma(-lrc, l1, x[1]);
+      }
+    }
+  }
+  return fail;
+}
+
+// ---------------------------------------------------------------------------
+// potrf team kernel
+
+template <int TW, int MAXT>
+__global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems) {
+  extern __shared__ __align__(128) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int team = warp / TW, tw = warp % TW;
+  const int teams_per_cta = (blockDim.x >> 5) / TW;
+  const int tthreads = TW * 32, ttid = tw * 32 + lane;
+  const int bar = 1 + team;
+  const int m = (int)g.m, n = (int)g.n;
+  Tri t;
+  t.cn8 = (n + 7) / 8 * 8;
+  t.gn = t.cn8 / 8;
+  const int gm = (m + 7) / 8;
+  const int tri_elems = (int)Tri::size(m, n);
+  double *S = smem + (ix)team * team_elems;
+  double *dinv = S + tri_elems;                        // cn8 doubles
+  volatile int *flag = (volatile int *)(dinv + t.cn8);  // failure index
+  const int fr = lane >> 2, fc = lane & 3;
+  const bool aligned_out = (g.di & 3) == 0;
+
+  for (ix b = (ix)blockIdx.x * teams_per_cta + team; b < g.batch; b += (ix)gridDim.x * teams_per_cta) {
+    if (g.merge && g.info[b] >= 0) continue;
+    const double *C = g.C.item(b);
+    // 1. lower trapezoid of C -> shared (zeros elsewhere in the tri layout)
+    for (int gg = 0; gg < gm; ++gg) {
+      const int w = t.width(gg), base = t.group_off(gg);
+      for (int q = ttid; q < 8 * w; q += tthreads) {
+        const int half = q / (4 * w), rem = q - half * 4 * w;
+        const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
+        double v = 0.0;
+        if (r < m && c < n && c <= r) v = C[eo(g.ci + r, g.cj + c, g.C.cn)];
+        S[base + q] = v;
+      }
+    }
+    if (ttid == 0) *flag = -1;
+    team_sync(bar, tthreads);
+
+    int fail = -1;
+    for (int jb = 0; jb < t.gn; ++jb) {
+      const int ncol = min(8, n - 8 * jb);
+      double acc[MAXT][2];
+      // downdate every row-group tile of this column block this warp owns
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int gg = jb + tw + u * TW;
+        if (gg < gm) {
+          acc[u][0] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc)];
+          acc[u][1] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc + 1)];
+          const int fa = tri_frag(t, gg, 0, lane), fb = tri_frag(t, jb, 0, lane);
+          for (int kk = 0; kk < 2 * jb; ++kk) dmma(acc[u], -S[fa + 16 * kk], S[fb + 16 * kk]);
+        }
+      }
+      // diagonal tile (owned by tw == 0, u == 0)
+      if (tw == 0) {
+        const int f = factor_diag_tile(acc[0], ncol, dinv + 8 * jb, lane);
+        // store the finished columns of the diagonal tile
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * fc + e;
+          if (c < ncol && (f < 0 || c < f)) S[t.off(8 * jb + fr, 8 * jb + c)] = acc[0][e];
+        }
+        if (f >= 0 && lane == 0) *flag = 8 * jb + f;
+      }
+      team_sync(bar, tthreads);
+      fail = *flag;
+      if (fail >= 0) break;
+      // solve the tiles below the diagonal
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int gg = jb + tw + u * TW;
+        if (gg < gm && gg > jb) {
+          solve_tile_rt(acc[u], S, t, jb, dinv, ncol, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 2 * fc + e;
+            if (c < ncol) S[t.off(8 * gg + fr, 8 * jb + c)] = acc[u][e];
+          }
+        }
+      }
+      team_sync(bar, tthreads);
+    }
+
+    // 3. write back: the lower trapezoid (or, on failure, exactly what the
+    // reference's block-row order would have stored, ccore.pyx:884-899)
+    double *D = g.D.item(b);
+    const int iif = fail >= 0 ? (fail & ~3) : 0;
+    if (fail < 0 || aligned_out) {
+      for (int gg = 0; gg < gm; ++gg) {
+        const int w = t.width(gg), base = t.group_off(gg);
+        for (int q = ttid; q < 8 * w; q += tthreads) {
+          const int half = q / (4 * w), rem = q - half * 4 * w;
+          const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
+          bool st = r < m && c < n && c <= r;
+          if (fail >= 0) st = st && (r < iif || (r < iif + 4 && c < iif));
+          if (st) D[eo(g.di + r, g.dj + c, g.D.cn)] = S[base + q];
+        }
+      }
+    }
+    double *dA = g.D.ditem(b);
+    const int nd = fail >= 0 ? fail : n;
+    for (int c = ttid; c < nd; c += tthreads) dA[g.dj + c] = dinv[c];
+    if (ttid == 0 && g.info) g.info[b] = fail >= 0 ? fail + g.info_offset : -1;
+    team_sync(bar, tthreads);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// trsm_rltn team kernel: D * A^T = alpha * B
+
+template <int TW>
+__global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_elems) {
+  extern __shared__ __align__(128) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int team = warp / TW, tw = warp % TW;
+  const int teams_per_cta = (blockDim.x >> 5) / TW;
+  const int tthreads = TW * 32, ttid = tw * 32 + lane;
+  const int bar = 1 + team;
+  const int m = (int)g.m, n = (int)g.n;
+  Tri t;
+  t.cn8 = (n + 7) / 8 * 8;
+  t.gn = t.cn8 / 8;
+  const int tri_elems = (int)Tri::size(n, n);
+  double *S = smem + (ix)team * team_elems;
+  double *dinv = S + tri_elems;
+  volatile int *flag = (volatile int *)(dinv + t.cn8);
+  double *strip = dinv + t.cn8 + 8 + tw * 8 * t.cn8;  // this warp's solved rows, 2 panels x cn8
+  const int fr = lane >> 2, fc = lane & 3;
+  const int gmr = (m + 7) / 8;
+
+  for (ix b = (ix)blockIdx.x * teams_per_cta + team; b < g.batch; b += (ix)gridDim.x * teams_per_cta) {
+    if (g.skip && g.skip[b] >= 0) continue;
+    const double *A = g.A.item(b);
+    for (int gg = 0; gg < t.gn; ++gg) {
+      const int w = t.width(gg), base = t.group_off(gg);
+      for (int q = ttid; q < 8 * w; q += tthreads) {
+        const int half = q / (4 * w), rem = q - half * 4 * w;
+        const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
+        double v = 0.0;
+        if (r < n && c <= r) v = A[eo(g.ai + r, g.aj + c, g.A.cn)];
+        S[base + q] = v;
+      }
+    }
+    if (ttid == 0) *flag = -1;
+    team_sync(bar, tthreads);
+    // reciprocals: reuse the factorization's, or compute (zero -> info)
+    if (g.use_dA) {
+      const double *dA = g.A.ditem(b);
+      for (int c = ttid; c < n; c += tthreads) dinv[c] = dA[g.aj + c];
+    } else {
+      for (int c = ttid; c < n; c += tthreads) dinv[c] = 1.0 / S[t.off(c, c)];
+    }
+    team_sync(bar, tthreads);
+    // first zero pivot (level3.py:171-175): the item is then left untouched
+    int fail = -1;
+    if (!g.use_dA) {
+      for (int c = 0; c < n; ++c)
+        if (S[t.off(c, c)] == 0.0) { fail = c; break; }
+    }
+    if (fail < 0) {
+      const double *B = g.B.item(b);
+      double *D = g.D.item(b);
+      for (int gg = tw; gg < gmr; gg += TW) {
+        for (int jb = 0; jb < t.gn; ++jb) {
+          const int ncol = min(8, n - 8 * jb);
+          double x[2];
+          const int r = 8 * gg + fr;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * jb + 2 * fc + e;
+            x[e] = (r < m && c < n) ? __dmul_rn(g.alpha, B[eo(g.bi + r, g.bj + c, g.B.cn)]) : 0.0;
+          }
+          const int fa = (lane >> 4) * 4 * t.cn8 + 4 * fc + ((lane >> 2) & 3);
+          const int fb = tri_frag(t, jb, 0, lane);
+          for (int kk = 0; kk < 2 * jb; ++kk) dmma(x, -strip[fa + 16 * kk], S[fb + 16 * kk]);
+          solve_tile_rt(x, S, t, jb, dinv, ncol, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * jb + 2 * fc + e;
+            strip[((fr >> 2) * 4 * t.cn8) + 4 * c + (fr & 3)] = x[e];
+            if (r < m && c < n) D[eo(g.di + r, g.dj + c, g.D.cn)] = x[e];
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (ttid == 0 && g.info) g.info[b] = fail;
+    team_sync(bar, tthreads);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host dispatch
+
+static int pick_teams(int tw, ix team_elems, int &threads, size_t &smem) {
+  int teams = 8 / tw;
+  if (teams < 1) teams = 1;
+  const size_t cap = 200 * 1024;
+  while (teams > 1 && (size_t)teams * team_elems * sizeof(double) > cap) --teams;
+  threads = teams * tw * 32;
+  smem = (size_t)teams * team_elems * sizeof(double);
+  return teams;
+}
+
+template <int TW, int MAXT>
+static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
+  auto kern = potrf_team_kernel<TW, MAXT>;
+  const ix cn8 = (g.n + 7) / 8 * 8;
+  ix team_elems = Tri::size(g.m, g.n) + cn8 + 8;
+  team_elems = (team_elems + 15) / 16 * 16;
+  int threads;
+  size_t smem;
+  const int teams = pick_teams(TW, team_elems, threads, smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  if (occ < 1) occ = 1;
+  ix grid = (g.batch + teams - 1) / teams;
+  const ix cap = (ix)num_sms() * occ;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems);
+  note_launch();
+  return cudaGetLastError();
+}
+
+bool potrf_fits(ix m, ix n) {
+  const ix cn8 = (n + 7) / 8 * 8;
+  const ix e = Tri::size(m, n) + cn8 + 8;
+  const ix gm = (m + 7) / 8;
+  return e * 8 <= 220 * 1024 && gm <= 8 * 8;
+}
+
+cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
+  const ix gm = (g.m + 7) / 8;
+  if (gm <= 2) return launch_potrf<1, 2>(g, st);
+  if (gm <= 4) return launch_potrf<1, 4>(g, st);
+  if (gm <= 8) return launch_potrf<4, 2>(g, st);
+  if (gm <= 16) return launch_potrf<8, 2>(g, st);
+  if (gm <= 32) return launch_potrf<8, 4>(g, st);
+  return launch_potrf<8, 8>(g, st);
+}
+
+bool trsm_fits(ix m, ix n) {
+  (void)m;
+  const ix cn8 = (n + 7) / 8 * 8;
+  const ix e = Tri::size(n, n) + cn8 + 8 + 8 * 8 * cn8;
+  return e * 8 <= 220 * 1024;
+}
+
+template <int TW>
+static cudaError_t launch_trsm(const TrsmArgs &g, cudaStream_t st) {
+  auto kern = trsm_team_kernel<TW>;
+  const ix cn8 = (g.n + 7) / 8 * 8;
+  ix team_elems = Tri::size(g.n, g.n) + cn8 + 8 + (ix)TW * 8 * cn8;
+  team_elems = (team_elems + 15) / 16 * 16;
+  int threads;
+  size_t smem;
+  const int teams = pick_teams(TW, team_elems, threads, smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  if (occ < 1) occ = 1;
+  ix grid = (g.batch + teams - 1) / teams;
+  const ix cap = (ix)num_sms() * occ;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// first zero on the diagonal of each item's n x n window (level3.py:171-175)
+__global__ void diag_check_kernel(Mat A, ix ai, ix aj, ix n, ix batch, int32_t *info) {
+  for (ix b = (ix)blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += (ix)gridDim.x * blockDim.x) {
+    const double *p = A.item(b);
+    int f = -1;
+    for (ix j = 0; j < n; ++j)
+      if (p[eo(ai + j, aj + j, A.cn)] == 0.0) { f = (int)j; break; }
+    info[b] = f;
+  }
+}
+
+cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *info, cudaStream_t st) {
+  ix blocks = (batch + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  diag_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, ai, aj, n, batch, info);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t run_trsm_rltn(const TrsmArgs &g, cudaStream_t st) {
+  const ix gmr = (g.m + 7) / 8;
+  if (gmr <= 1) return launch_trsm<1>(g, st);
+  if (gmr <= 2) return launch_trsm<2>(g, st);
+  if (gmr <= 4) return launch_trsm<4>(g, st);
+  return launch_trsm<8>(g, st);
+}
+
+}  // namespace pb

@@ -1,0 +1,364 @@
+// Batched dgemm_nt / dsyrk_ln on panel-major FP64 storage (sm_100a).
+//
+// Reference semantics: gemm_nt_drv ccore.pyx:746-771 (+ _store_block
+// :26-42), syrk_ln_drv ccore.pyx:804-831 (+ _ksyrk_core :275-293).
+//
+// Two kernel families, both on the FP64 tensor path (mma.sync m8n8k4 f64,
+// SASS DMMA.8x8x4; on B200 DMMA and DFMA share the same 37 TF/s peak, see
+// profiles/r01_fp64_peak.log, but DMMA needs 1/8 of the issue slots and
+// shares each fragment across an 8x8 tile instead of re-reading it):
+//
+//  * gemm_direct: one warp per item for tiny items (m, n <= 24).  The
+//    panel-major layout makes every A/B fragment two contiguous 128-byte
+//    runs, so fragments are read straight from HBM, fully coalesced, with
+//    no shared-memory staging at all.
+//  * gemm_tiled: persistent CTAs stream (item, tile, k-chunk) steps
+//    through a cp.async multi-stage shared-memory pipeline that crosses
+//    item boundaries, so the next item's operands are in flight while the
+//    current item's epilogue drains.
+//
+// Both honour the reference's discrete semantics exactly: alpha == 0
+// never touches A/B (NaN-safe), beta == 0 never reads C, writes stay in
+// the m x n window (syrk: lower triangle only), unaligned row origins are
+// gathered in-kernel instead of the reference's host repack
+// (level3.py:56-62).
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+// _store_block rule (ccore.pyx:26-42); no contraction so alpha=1/beta=0
+// and the special cases are exact.
+__device__ __forceinline__ double store_rule(double alpha, double acc, double beta, double c) {
+  if (alpha != 0.0) {
+    double v = __dmul_rn(alpha, acc);
+    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c));
+    return v;
+  }
+  return beta != 0.0 ? __dmul_rn(beta, c) : 0.0;
+}
+// _ksyrk_core diagonal-tile rule (ccore.pyx:288-292).
+__device__ __forceinline__ double syrk_diag_rule(double alpha, double acc, double beta, double c) {
+  double v = beta != 0.0 ? __dmul_rn(beta, c) : 0.0;
+  if (alpha != 0.0) v = __dadd_rn(__dmul_rn(alpha, acc), v);
+  return v;
+}
+
+template <bool SYRK>
+__device__ __forceinline__ bool in_store(ix r, ix c, ix m, ix n) {
+  return r < m && c < n && (!SYRK || r >= c);
+}
+
+template <bool SYRK>
+__device__ __forceinline__ double epilogue_value(const GemmArgs &g, ix r, ix c, double acc, double cv) {
+  if (SYRK && ((r >> 2) == (c >> 2))) return syrk_diag_rule(g.alpha, acc, g.beta, cv);
+  return store_rule(g.alpha, acc, g.beta, cv);
+}
+
+// ---------------------------------------------------------------------------
+// gemm_direct: warp per item, fragments straight from global memory.
+
+template <int MT, int NT, bool SYRK>
+__global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g) {
+  const int lane = threadIdx.x & 31;
+  const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const ix nwarps = (ix)gridDim.x * (blockDim.x >> 5);
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row / k-col
+  for (ix b = warp; b < g.batch; b += nwarps) {
+    if (g.skip && g.skip[b] >= 0) continue;
+    const double *A = g.A.item(b);
+    const double *B = g.B.item(b);
+    const double *C = g.C.item(b);
+    double *D = g.D.item(b);
+    double cv[MT][NT][2];
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          acc[i][j][e] = 0.0;
+          cv[i][j][e] = 0.0;
+          const ix r = 8 * i + fr, c = 8 * j + 2 * fc + e;
+          if (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n)) cv[i][j][e] = C[eo(g.ci + r, g.cj + c, g.C.cn)];
+        }
+    if (g.alpha != 0.0) {
+      for (int k0 = 0; k0 < g.k; k0 += 4) {
+        const int l = k0 + fc;
+        double a[MT], bb[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const ix r = 8 * i + fr;
+          a[i] = (r < g.m && l < g.k) ? ldg_nc(A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const ix r = 8 * j + fr;
+          bb[j] = (r < g.n && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+            if (!SYRK || j <= i) dmma(acc[i][j], a[i], bb[j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const ix r = 8 * i + fr, c = 8 * j + 2 * fc + e;
+          if (in_store<SYRK>(r, c, g.m, g.n))
+            D[eo(g.di + r, g.dj + c, g.D.cn)] = epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
+        }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gemm_tiled: persistent, cp.async multi-stage pipeline over
+// (unit = item x output tile, k-chunk) steps.
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES>
+struct TiledCfg {
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NWARPS = WARPS_M * WARPS_N;
+  static constexpr int NTHREADS = 32 * NWARPS;
+  static constexpr int MT = WM / 8, NT = WN / 8;
+  static constexpr int A_ELEMS = BM * KC, B_ELEMS = BN * KC;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES;
+};
+
+// Load a (ROWS x KC) panel tile of window rows [r0, r0+ROWS), cols
+// [l0, l0+KC) into shared memory (panel-major, panel length KC).
+// Rows >= rows_valid and cols >= k are zero-filled without reading.
+template <int ROWS, int KC, int NTHREADS>
+__device__ __forceinline__ void load_panel_tile(double *s, const double *G, ix cn, ix gi, ix gj, ix r0, ix l0,
+                                                ix rows_valid, ix k, bool vec16) {
+  if (vec16) {
+    // 16-byte pieces: (panel p, col l, half h) -> rows 4p+2h, 4p+2h+1.
+    constexpr int PIECES = (ROWS / 4) * KC * 2;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < PIECES; q += NTHREADS) {
+      const int p = q / (2 * KC), w = q % (2 * KC), l = w >> 1, h = w & 1;
+      const ix R = r0 + 4 * p + 2 * h, L = l0 + l;
+      const bool ok = R < rows_valid && L < k;
+      const double *src = ok ? G + eo(gi + R, gj + L, cn) : G;
+      cp_async16(s + p * 4 * KC + 4 * l + 2 * h, src, ok ? 16 : 0);
+    }
+  } else {
+    constexpr int ELEMS = ROWS * KC;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < ELEMS; q += NTHREADS) {
+      const int p = q / (4 * KC), w = q % (4 * KC), l = w >> 2, rr = w & 3;
+      const ix R = r0 + 4 * p + rr, L = l0 + l;
+      const bool ok = R < rows_valid && L < k;
+      const double *src = ok ? G + eo(gi + R, gj + L, cn) : G;
+      cp_async8(s + p * 4 * KC + 4 * l + rr, src, ok ? 8 : 0);
+    }
+  }
+}
+
+__device__ __forceinline__ void unit_coords(ix u, ix tiles_m, ix tiles_n, bool syrk, ix &b, ix &tm, ix &tn) {
+  if (!syrk) {
+    const ix per = tiles_m * tiles_n;
+    b = u / per;
+    const ix t = u % per;
+    tm = t / tiles_n;
+    tn = t % tiles_n;
+  } else {
+    const ix per = tiles_m * (tiles_m + 1) / 2;
+    b = u / per;
+    ix t = u % per;
+    // lower-triangular tile index -> (tm, tn), tn <= tm
+    ix r = (ix)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (r * (r + 1) / 2 > t) --r;
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    tm = r;
+    tn = t - r * (r + 1) / 2;
+  }
+}
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
+__global__ void __launch_bounds__(TiledCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS)
+    gemm_tiled_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
+  using Cfg = TiledCfg<BM, BN, WM, WN, KC, STAGES>;
+  constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  extern __shared__ __align__(128) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int fr = lane >> 2, fc = lane & 3;
+
+  const ix nk = g.alpha != 0.0 ? (g.k + KC - 1) / KC : 0;
+  const ix steps_per_unit = nk > 0 ? nk : 1;
+  const ix my_units = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const ix nsteps = my_units * steps_per_unit;
+  const bool vecA = g.vecA, vecB = g.vecB;
+
+  auto issue = [&](ix s) {
+    const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
+    const ix ch = s % steps_per_unit;
+    ix b, tm, tn;
+    unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+    double *st = smem + (s % STAGES) * Cfg::STAGE_ELEMS;
+    load_panel_tile<BM, KC, Cfg::NTHREADS>(st, g.A.item(b), g.A.cn, g.ai, g.aj, tm * BM, ch * KC, g.m, g.k, vecA);
+    load_panel_tile<BN, KC, Cfg::NTHREADS>(st + Cfg::A_ELEMS, g.B.item(b), g.B.cn, g.bi, g.bj, tn * BN, ch * KC,
+                                           SYRK ? g.m : g.n, g.k, vecB);
+  };
+
+  if (nk > 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nsteps) issue(s);
+      cp_async_commit();
+    }
+  }
+
+  double acc[MT][NT][2];
+  double cv[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (ix s = 0; s < nsteps; ++s) {
+    const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
+    const ix ch = s % steps_per_unit;
+    ix b, tm, tn;
+    unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+    const ix rbase = tm * BM + wm * WM, cbase = tn * BN + wn * WN;
+    if (ch == 0 && g.beta != 0.0) {
+      // prefetch this unit's C fragments; consumed in the epilogue
+      const double *C = g.C.item(b);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+            cv[i][j][e] = in_store<SYRK>(r, c, g.m, g.n) ? ldg_nc(C + eo(g.ci + r, g.cj + c, g.C.cn)) : 0.0;
+          }
+    }
+    if (nk > 0) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      if (s + STAGES - 1 < nsteps) issue(s + STAGES - 1);
+      cp_async_commit();
+      const double *sa = smem + (s % STAGES) * Cfg::STAGE_ELEMS + (wm * WM / 4) * 4 * KC;
+      const double *sb = smem + (s % STAGES) * Cfg::STAGE_ELEMS + Cfg::A_ELEMS + (wn * WN / 4) * 4 * KC;
+      const bool active = !SYRK || (cbase <= rbase + WM - 1);
+      if (active) {
+        const int foff = (lane >> 4) * 4 * KC + 4 * fc + (fr & 3);
+#pragma unroll
+        for (int kk = 0; kk < KC / 4; ++kk) {
+          double a[MT], bb[NT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) a[i] = sa[i * 8 * KC + 16 * kk + foff];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) bb[j] = sb[j * 8 * KC + 16 * kk + foff];
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], bb[j]);
+        }
+      }
+    }
+    if (ch == steps_per_unit - 1) {
+      double *D = g.D.item(b);
+      const bool skip = g.skip && g.skip[b] >= 0;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+            if (!skip && in_store<SYRK>(r, c, g.m, g.n))
+              D[eo(g.di + r, g.dj + c, g.D.cn)] =
+                  epilogue_value<SYRK>(g, r, c, acc[i][j][e], g.beta != 0.0 ? cv[i][j][e] : 0.0);
+            acc[i][j][e] = 0.0;
+          }
+    }
+  }
+  if (nk > 0) cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// host dispatch
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int MT, int NT, bool SYRK>
+static cudaError_t launch_direct(const GemmArgs &g, cudaStream_t st) {
+  const int threads = 256;
+  const ix warps_needed = g.batch;
+  ix blocks = (warps_needed + 7) / 8;
+  const ix cap = (ix)num_sms() * 8 * 8;  // ~8 resident CTAs of 8 warps per SM, a few waves
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  gemm_direct_kernel<MT, NT, SYRK><<<(unsigned)blocks, threads, 0, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <bool SYRK>
+static cudaError_t dispatch_direct(const GemmArgs &g, cudaStream_t st) {
+  const int mt = (int)((g.m + 7) / 8), nt = (int)(((SYRK ? g.m : g.n) + 7) / 8);
+#define PB_DIRECT(M_, N_) \
+  if (mt == M_ && nt == N_) return launch_direct<M_, N_, SYRK>(g, st);
+  PB_DIRECT(1, 1) PB_DIRECT(1, 2) PB_DIRECT(1, 3) PB_DIRECT(2, 1) PB_DIRECT(2, 2) PB_DIRECT(2, 3)
+  PB_DIRECT(3, 1) PB_DIRECT(3, 2) PB_DIRECT(3, 3)
+#undef PB_DIRECT
+  return cudaErrorInvalidValue;
+}
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
+static cudaError_t launch_tiled(const GemmArgs &g, cudaStream_t st) {
+  using Cfg = TiledCfg<BM, BN, WM, WN, KC, STAGES>;
+  auto kern = gemm_tiled_kernel<BM, BN, WM, WN, KC, STAGES, SYRK>;
+  static bool configured = false;
+  static int occ = 1;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
+    if (occ < 1) occ = 1;
+    configured = true;
+  }
+  const ix tiles_m = (g.m + BM - 1) / BM;
+  const ix tiles_n = SYRK ? tiles_m : (g.n + BN - 1) / BN;
+  const ix per = SYRK ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  const ix nunits = per * g.batch;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > nunits) grid = nunits;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, Cfg::NTHREADS, Cfg::SMEM, st>>>(g, tiles_m, tiles_n, nunits);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <bool SYRK>
+static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
+  const ix ncols = SYRK ? g.m : g.n;
+  const ix big = g.m > ncols ? g.m : ncols;
+  if (big <= 24) return dispatch_direct<SYRK>(g, st);
+  const ix small = g.m < ncols ? g.m : ncols;
+  if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);
+  return launch_tiled<64, 64, 32, 32, 32, 2, SYRK>(g, st);
+}
+
+cudaError_t run_gemm_nt(const GemmArgs &g, cudaStream_t st) { return dispatch_gemm<false>(g, st); }
+cudaError_t run_syrk_ln(const GemmArgs &g, cudaStream_t st) { return dispatch_gemm<true>(g, st); }
+
+}  // namespace pb

@@ -1,0 +1,66 @@
+// Internal launch-argument structs shared by the kernels and the C ABI.
+#pragma once
+#include "pb_common.cuh"
+
+namespace pb {
+
+struct GemmArgs {
+  ix m, n, k;
+  double alpha, beta;
+  Mat A, B, C, D;
+  ix ai, aj, bi, bj, ci, cj, di, dj;
+  ix batch;
+  bool vecA, vecB;      // 16-byte cp.async legal for the A / B stream
+  const int32_t *skip;  // optional: item b is left untouched if skip[b] >= 0
+};
+
+struct TrsmArgs {
+  ix m, n;
+  double alpha;
+  Mat A, B, D;
+  ix ai, aj, bi, bj, di, dj;
+  int use_dA;
+  int32_t *info;
+  ix batch;
+  const int32_t *skip;  // optional: item b is left untouched if skip[b] >= 0
+};
+
+struct PotrfArgs {
+  ix m, n;
+  Mat C, D;
+  ix ci, cj, di, dj;
+  int32_t *info;
+  ix batch;
+  // merge mode (blocked driver): items with info[b] >= 0 on entry are
+  // skipped; a new failure is stored as info_offset + local index.
+  int merge;
+  int info_offset;
+};
+
+struct CopyArgs {
+  ix m, n;
+  // strided (dense) side
+  const double *X;
+  double *Xw;
+  ix x_row, x_col, x_stride;
+  // panel sides
+  Mat S, D;
+  ix si, sj, di, dj;
+  ix batch;
+};
+
+void note_launch();
+int num_sms();
+
+cudaError_t run_gemm_nt(const GemmArgs &g, cudaStream_t st);
+cudaError_t run_syrk_ln(const GemmArgs &g, cudaStream_t st);
+cudaError_t run_trsm_rltn(const TrsmArgs &g, cudaStream_t st);
+cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st);
+cudaError_t run_pack(const CopyArgs &g, cudaStream_t st);
+cudaError_t run_unpack(const CopyArgs &g, cudaStream_t st);
+cudaError_t run_gecp(const CopyArgs &g, cudaStream_t st);
+cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *info, cudaStream_t st);
+bool potrf_fits(ix m, ix n);
+bool trsm_fits(ix m, ix n);
+
+}  // namespace pb

@@ -1,0 +1,210 @@
+"""Batched level-3 routines on panel-major batches: the reference's
+``level3`` API (level3.py:81-350) with every operand a batch.
+
+Same names, argument order, bounds checks, error types and discrete
+semantics as the reference:
+
+* ``gemm_nt(m, n, k, alpha, A, B, beta, C, D)``      level3.py:81-98
+* ``syrk_ln(m, k, alpha, A, B, beta, C, D)``         level3.py:120-137
+* ``trsm_rltn(m, n, alpha, A, B, D)``                level3.py:220-221, 180-244
+* ``potrf_l(m, C, D, n=None)``                       level3.py:319-350
+
+Operands are :class:`PanelBatch` objects or :class:`SubRef` windows into
+them; an operand with batch 1 broadcasts to D's batch.  All work is
+enqueued on the current torch CUDA stream through the C ABI
+(include/pb_b200.h); the only host synchronisation is the optional
+pivot check of the factorizations (``check=True``, the reference's
+raise-on-bad-pivot behaviour).  Per-item statuses are returned as an
+int32 device tensor ``info`` (-1 ok, else first failing index), and a
+failing item is handled exactly like an independent reference call:
+the other items are still computed.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from .errors import DimensionError, NotPositiveDefiniteError, SingularMatrixError
+from .matstore import PanelBatch, SubRef
+
+TRSM_VARIANTS = ("llnu", "lunn", "rltn", "rltu", "rutn")
+
+
+def _ref(x, name):
+    if isinstance(x, PanelBatch):
+        return x, 0, 0
+    if isinstance(x, SubRef) and isinstance(x.mat, PanelBatch):
+        return x.mat, x.ai, x.aj
+    raise TypeError(f"{name} must be a PanelBatch or a panel SubRef")
+
+
+def _check(mat, ai, aj, m, n, name):
+    # level3.py:47-53
+    if m < 0 or n < 0:
+        raise DimensionError(f"negative size {m}x{n} for {name}")
+    if ai + m > mat.rows or aj + n > mat.cols:
+        raise DimensionError(
+            f"{name} window ({ai}:{ai + m}, {aj}:{aj + n}) exceeds "
+            f"{mat.rows}x{mat.cols} matrix")
+
+
+def _batch_of(d, *inputs):
+    nb = d.batch
+    for x in inputs:
+        if x.batch not in (nb, 1):
+            raise DimensionError(f"operand batch {x.batch} does not match output batch {nb}")
+        if x.device != d.device:
+            raise DimensionError("operands live on different devices")
+    if d.device.type != "cuda":
+        raise RuntimeError("panel-major engine runs on CUDA devices only (no CPU fallback)")
+    return nb
+
+
+def _stream(dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _mark_diag(mat, dj, n, diagonal):
+    # level3.py:69-74
+    if diagonal:
+        mat.diag_lo = dj
+        mat.diag_hi = dj + n
+    else:
+        mat.diag_lo = mat.diag_hi = 0
+
+
+def _first_failure(info):
+    """(batch_index, index) of the first failing item, or None (host sync)."""
+    bad = torch.nonzero(info >= 0)
+    if bad.numel() == 0:
+        return None
+    b = int(bad[0, 0])
+    return b, int(info[b])
+
+
+# ---------------------------------------------------------------------------
+# gemm / syrk
+
+
+def gemm_nt(m, n, k, alpha, A, B, beta, C, D):
+    """D = alpha*A*B' + beta*C with A m x k and B n x k, for every item."""
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, m, k, "A")
+    _check(b, bi, bj, n, k, "B")
+    _check(c, ci, cj, m, n, "C")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, a, b, c)
+    if m == 0 or n == 0 or nb == 0:
+        return
+    da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
+    _native.call("pb_dgemm_nt", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+
+
+def syrk_ln(m, k, alpha, A, B, beta, C, D):
+    """Lower triangle of D = alpha*A*B' + beta*C (m x m); upper untouched."""
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, m, k, "A")
+    _check(b, bi, bj, m, k, "B")
+    _check(c, ci, cj, m, m, "C")
+    _check(d, di, dj, m, m, "D")
+    nb = _batch_of(d, a, b, c)
+    if m == 0 or nb == 0:
+        return
+    da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
+    _native.call("pb_dsyrk_ln", m, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+
+
+# ---------------------------------------------------------------------------
+# triangular solve
+
+
+def trsm(m, n, alpha, A, B, D, variant, check=True):
+    """Variant dispatcher of the reference (level3.py:180-209); only the
+    hot-path variant ``rltn`` is provided by this engine."""
+    if variant not in TRSM_VARIANTS:
+        raise ValueError(f"unknown trsm variant {variant!r}; one of {TRSM_VARIANTS}")
+    if variant != "rltn":
+        raise NotImplementedError(f"trsm variant {variant!r} is outside the batched hot path (rltn only)")
+    return trsm_rltn(m, n, alpha, A, B, D, check=check)
+
+
+def trsm_rltn(m, n, alpha, A, B, D, check=True):
+    """Solve D*A' = alpha*B, A n x n lower non-unit, for every item.
+
+    Reciprocals follow level3._recip_diag (level3.py:160-177): the
+    factorization's diag_inv is reused when the A window sits on the
+    diagonal of A's freshly factored range, otherwise 1/A[j,j] is computed
+    in-kernel and an item with a zero pivot is left untouched.  Returns the
+    per-item ``info`` tensor (or None when reciprocals were reused); with
+    ``check`` a zero pivot raises SingularMatrixError like the reference.
+    """
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, n, n, "A")
+    _check(b, bi, bj, m, n, "B")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, a, b)
+    if m == 0 or n == 0 or nb == 0:
+        return None
+    use_dA = 1 if (ai == aj and a.diag_inv_valid(aj, n)) else 0
+    info = None if use_dA else torch.empty(nb, dtype=torch.int32, device=d.device)
+    da, db, dd = (x.descriptor(nb) for x in (a, b, d))
+    _native.call("pb_dtrsm_rltn", m, n, float(alpha), ctypes.byref(da), ai, aj, use_dA, ctypes.byref(db), bi, bj,
+                 ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr() if info is not None else 0),
+                 _stream(d.device))
+    if check and info is not None:
+        f = _first_failure(info)
+        if f is not None:
+            raise SingularMatrixError(f"trsm_rlt: zero diagonal at column {f[1]} (batch item {f[0]})",
+                                      f[1], batch_index=f[0], info=info)
+    return info
+
+
+# ---------------------------------------------------------------------------
+# Cholesky
+
+
+def potrf_l(m, C, D, n=None, check=True):
+    """Lower Cholesky factor of every item's lower(C) into D (level3.py:319-350).
+
+    n < m factors the top n x n block and solves the trailing rows against
+    it.  Fills D.diag_inv[:, dj:dj+n].  Returns the per-item ``info``
+    tensor; with ``check`` the first bad pivot raises
+    NotPositiveDefiniteError (index relative to the window, plus
+    batch_index) after all items have been processed.
+    """
+    if n is None:
+        n = m
+    if n > m:
+        raise DimensionError(f"potrf_l needs n <= m, got m={m} n={n}")
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(c, ci, cj, m, n, "C")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, c)
+    if n == 0 or nb == 0:
+        return None
+    info = torch.empty(nb, dtype=torch.int32, device=d.device)
+    dc, dd = c.descriptor(nb), d.descriptor(nb)
+    _native.call("pb_dpotrf_l", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj,
+                 ctypes.c_void_p(info.data_ptr()), _stream(d.device))
+    if check:
+        f = _first_failure(info)
+        if f is not None:
+            _mark_diag(d, dj, 0, False)
+            raise NotPositiveDefiniteError(
+                f"potrf_l: non-positive pivot at index {f[1]} (batch item {f[0]})", f[1],
+                batch_index=f[0], info=info)
+    _mark_diag(d, dj, n, di == dj)
+    return info

@@ -1,0 +1,461 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+* every golden case recorded from the reference, run as a batch;
+* seeded random batches at every kernel-dispatch regime (direct,
+  tiled-32, tiled-64, team sizes, blocked composites) against the
+  oracle (pinned bit-exact to the reference in test_oracle.py);
+* the reference's discrete semantics (alpha/beta/k/m/n zero cases,
+  windows never left, aliasing bit-equal, determinism, failure indices
+  and partial writes), all exact;
+* full BASELINE-size batches through size-independent properties.
+
+Tolerance (north_star): relative Frobenius error <= 50 * n * eps_fp64 on
+floating-point results; bit-exact for pack/unpack/copies, untouched
+storage and info.
+"""
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, load_golden
+from golden_util import host_inputs, out_labels, run_oracle, written_mask
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+torch = pytest.importorskip("torch")
+import paper_1704_02457_b200 as pb  # noqa: E402
+from paper_1704_02457_b200 import level3, pack  # noqa: E402
+
+EPS = np.finfo(np.float64).eps
+
+
+def dev(h):
+    """HostBatch -> PanelBatch on cuda:0 (same bytes)."""
+    t = torch.from_numpy(h.storage.copy()).cuda()
+    p = pb.create_panel_batch(h.batch, h.rows, h.cols, t)
+    p.diag_lo, p.diag_hi = h.diag_lo, h.diag_hi
+    return p
+
+
+def host(p):
+    return p.storage.detach().cpu().numpy()
+
+
+def fp_close(got, want, n, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    both_nan = np.isnan(got) & np.isnan(want)
+    assert not np.any(np.isnan(got) ^ np.isnan(want)), f"NaN pattern differs {what}"
+    d = np.where(both_nan, 0.0, got - want)
+    w = np.where(both_nan, 0.0, want)
+    den = np.linalg.norm(w)
+    err = np.linalg.norm(d) / den if den > 0 else np.linalg.norm(d)
+    assert err <= 50 * max(n, 1) * EPS, f"rel Frobenius {err:.3e} > {50 * max(n, 1) * EPS:.3e} {what}"
+
+
+def compare_storage(got, want, mask, n, what):
+    """mask True: FP tolerance; mask False: bit-exact."""
+    gu, wu = got.view(np.uint64), want.view(np.uint64)
+    assert np.array_equal(gu[..., ~mask], wu[..., ~mask]), f"untouched storage changed {what}"
+    fp_close(got[..., mask], want[..., mask], n, what)
+
+
+def run_product(case, mats):
+    p = case["params"]
+    op = case["op"]
+    if op == "gemm_nt":
+        level3.gemm_nt(p["m"], p["n"], p["k"], p["alpha"], mats["A"].ref(p["ai"], p["aj"]),
+                       mats["B"].ref(p["bi"], p["bj"]), p["beta"], mats["C"].ref(p["ci"], p["cj"]),
+                       mats["D"].ref(p["di"], p["dj"]))
+        return None
+    if op == "syrk_ln":
+        level3.syrk_ln(p["m"], p["k"], p["alpha"], mats["A"].ref(p["ai"], p["aj"]), mats["B"].ref(p["bi"], p["bj"]),
+                       p["beta"], mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]))
+        return None
+    if op == "trsm_rltn":
+        return level3.trsm_rltn(p["m"], p["n"], p["alpha"], mats["A"].ref(p["ai"], p["aj"]),
+                                mats["B"].ref(p["bi"], p["bj"]), mats["D"].ref(p["di"], p["dj"]), check=False)
+    if op == "potrf_l":
+        return level3.potrf_l(p["m"], mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]), n=p["n"],
+                              check=False)
+    raise ValueError(op)
+
+
+def dims_n(case):
+    p = case["params"]
+    return max(p.get("m", 1), p.get("n", 1), p.get("k", 1))
+
+
+@pytest.mark.parametrize("batch", [1, 5])
+def test_golden_cases(batch):
+    z, cases = load_golden()
+    for case in cases:
+        if case["op"] == "pack":
+            continue
+        hm = host_inputs(z, case, batch)
+        dm = {}
+        for lab, h in hm.items():
+            if lab not in case["alias"]:
+                dm[lab] = dev(h)
+        for lab, tgt in case["alias"].items():
+            dm[lab] = dm[tgt]
+        info = run_product(case, dm)
+        torch.cuda.synchronize()
+        if info is not None:
+            assert np.all(info.cpu().numpy() == case["status"]), (case["name"], info.cpu().numpy(), case["status"])
+        for lab in out_labels(case):
+            want = z[f"{case['key']}/out/{lab}"]
+            got = host(dm[lab])[:, : want.size]
+            h = hm[lab]
+            mask = written_mask(case, lab, want.size, h.cn, case["status"])
+            if case["op"] == "potrf_l" and lab == case["alias"].get("D", "D"):
+                mask[h.diag_off + case["params"]["dj"]: h.diag_off + case["params"]["dj"] + case["params"]["n"]] = True
+            for b in range(batch):
+                compare_storage(got[b], want, mask, dims_n(case), f"{case['name']}/{lab}/item{b}")
+
+
+# ---------------------------------------------------------------------------
+# random batches against the oracle
+
+
+def rand_batch(rng, nb, m, n, fill=None):
+    h = O.HostBatch(nb, m, n)
+    h.storage[:] = rng.uniform(-1, 1, h.storage.shape) if fill is None else fill
+    return h
+
+
+GEMM_SHAPES = [(4, 4, 4), (8, 8, 8), (12, 12, 12), (16, 16, 16), (20, 20, 20), (24, 24, 24), (3, 17, 5),
+               (28, 28, 28), (32, 32, 32), (40, 40, 40), (44, 36, 52), (64, 64, 64), (72, 72, 72), (100, 100, 100),
+               (128, 128, 128), (300, 300, 300), (65, 130, 7), (9, 70, 33)]
+
+
+@pytest.mark.parametrize("mnk", GEMM_SHAPES)
+def test_gemm_nt_random_vs_oracle(mnk):
+    m, n, k = mnk
+    rng = np.random.default_rng(m * 10007 + n * 101 + k)
+    nb = 3 if m >= 128 else 17
+    for (oa, ob, oc, od, alpha, beta) in [((0, 0), (0, 0), (0, 0), (0, 0), 1.0, 1.0),
+                                          ((3, 1), (1, 2), (2, 0), (1, 3), -1.5, 0.5),
+                                          ((4, 0), (0, 4), (0, 0), (4, 1), 1.0, 0.0)]:
+        A = rand_batch(rng, nb, oa[0] + m + 1, oa[1] + k + 2)
+        B = rand_batch(rng, nb, ob[0] + n + 2, ob[1] + k + 1)
+        C = rand_batch(rng, nb, oc[0] + m, oc[1] + n)
+        D = rand_batch(rng, nb, od[0] + m + 3, od[1] + n + 1)
+        dA, dB, dC, dD = dev(A), dev(B), dev(C), dev(D)
+        level3.gemm_nt(m, n, k, alpha, dA.ref(*oa), dB.ref(*ob), beta, dC.ref(*oc), dD.ref(*od))
+        O.gemm_nt(m, n, k, alpha, A, *oa, B, *ob, beta, C, *oc, D, *od)
+        mask = np.zeros(D.per, dtype=bool)
+        for i in range(m):
+            for j in range(n):
+                mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+        compare_storage(host(dD), D.storage, mask, max(m, n, k), f"gemm {mnk} {oa}{od}")
+
+
+@pytest.mark.parametrize("mk", [(4, 3), (8, 8), (13, 5), (24, 24), (33, 17), (40, 40), (64, 64), (96, 40),
+                                (128, 64), (200, 31)])
+def test_syrk_ln_random_vs_oracle(mk):
+    m, k = mk
+    rng = np.random.default_rng(m * 31 + k)
+    nb = 9
+    for (oa, same, od, alpha, beta) in [((0, 0), False, (0, 0), 1.0, 1.0), ((3, 1), True, (0, 0), -1.0, 1.0),
+                                        ((3, 1), True, (3, 1), -1.0, 1.0), ((1, 0), False, (2, 2), 0.5, 0.0)]:
+        A = rand_batch(rng, nb, oa[0] + m + 2, oa[1] + k + 1)
+        B = A if same else rand_batch(rng, nb, m + 1, k + 2)
+        ob = oa if same else (0, 1)
+        if not same:
+            ob = (1, 1)
+            B = rand_batch(rng, nb, ob[0] + m, ob[1] + k)
+        C = rand_batch(rng, nb, m + 1, m + 2)
+        D = rand_batch(rng, nb, od[0] + m + 1, od[1] + m)
+        dA = dev(A)
+        dB = dA if same else dev(B)
+        dC, dD = dev(C), dev(D)
+        level3.syrk_ln(m, k, alpha, dA.ref(*oa), dB.ref(*ob), beta, dC.ref(1, 0), dD.ref(*od))
+        O.syrk_ln(m, k, alpha, A, *oa, B, *ob, beta, C, 1, 0, D, *od)
+        mask = np.zeros(D.per, dtype=bool)
+        for j in range(m):
+            for i in range(j, m):
+                mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+        compare_storage(host(dD), D.storage, mask, max(m, k), f"syrk {mk} {oa}{od}")
+
+
+def spd_batch(rng, nb, n, shift=None):
+    g = rng.uniform(-1, 1, (nb, n, n))
+    return g @ g.transpose(0, 2, 1) + (n if shift is None else shift) * np.eye(n)
+
+
+@pytest.mark.parametrize("mn", [(4, 4), (8, 8), (11, 11), (16, 16), (24, 24), (32, 32), (37, 37), (64, 64),
+                                (96, 96), (128, 128), (160, 160), (232, 232), (256, 256), (300, 300), (29, 13),
+                                (256, 128), (70, 33)])
+def test_potrf_l_random_vs_oracle(mn):
+    m, n = mn
+    rng = np.random.default_rng(m * 7 + n)
+    nb = 4 if m >= 128 else 13
+    for (oc, od) in [((0, 0), (0, 0)), ((3, 2), (4, 1)), ((1, 1), (1, 1))]:
+        a = spd_batch(rng, nb, m)[:, :, :n]
+        if m > n:
+            a[:, n:, :] = rng.uniform(-1, 1, (nb, m - n, n))
+        C = rand_batch(rng, nb, oc[0] + m + 1, oc[1] + n + 2)
+        C.set_window(oc[0], oc[1], a)
+        D = rand_batch(rng, nb, od[0] + m, od[1] + n + 1, fill=1.25)
+        dC, dD = dev(C), dev(D)
+        info = level3.potrf_l(m, dC.ref(*oc), dD.ref(*od), n=n, check=False)
+        winfo = O.potrf_l(m, C, *oc, D, *od, n=n)
+        assert np.array_equal(info.cpu().numpy(), winfo)
+        mask = np.zeros(D.per, dtype=bool)
+        for j in range(n):
+            for i in range(j, m):
+                mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+        mask[D.diag_off + od[1]: D.diag_off + od[1] + n] = True
+        compare_storage(host(dD), D.storage, mask, m, f"potrf {mn} {oc}{od}")
+
+
+@pytest.mark.parametrize("n", [4, 8, 12, 16, 24, 40, 64, 128])
+def test_potrf_failure_index_and_partial_writes(n):
+    """Bad pivots: info equals the reference's index, and the failing item is
+    written exactly as far as the reference writes it (ccore.pyx:884-899)."""
+    rng = np.random.default_rng(n)
+    nb = 16
+    a = spd_batch(rng, nb, n)
+    fails = rng.integers(0, n, nb)
+    for b in range(nb):
+        if b % 3 != 2:  # keep some items healthy
+            a[b, fails[b], fails[b]] = -10.0 * n
+    a[5, 0, 0] = np.nan  # NaN passes the d <= 0 test (ccore.pyx:423)
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    D = rand_batch(rng, nb, n, n, fill=2.5)
+    dC, dD = dev(C), dev(D)
+    info = level3.potrf_l(n, dC, dD, check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
+    assert np.array_equal(info, winfo)
+    got = host(dD)
+    for b in range(nb):
+        g, w = got[b], D.storage[b]
+        gn, wn = np.isnan(g), np.isnan(w)
+        assert np.array_equal(gn, wn), b
+        same = np.isclose(g, w, rtol=1e-11, atol=1e-11) | (gn & wn)
+        assert np.all(same), (b, info[b])
+    with pytest.raises(pb.NotPositiveDefiniteError) as ei:
+        level3.potrf_l(n, dC, dD)
+    first = int(np.nonzero(winfo >= 0)[0][0])
+    assert ei.value.batch_index == first and ei.value.index == winfo[first]
+    assert not dD.diag_inv_valid(0, n)
+
+
+@pytest.mark.parametrize("mn", [(2, 2), (5, 3), (8, 8), (3, 9), (13, 6), (72, 48), (40, 64), (33, 100), (16, 232),
+                                (24, 256), (9, 300)])
+def test_trsm_rltn_random_vs_oracle(mn):
+    m, n = mn
+    rng = np.random.default_rng(m * 3 + n)
+    nb = 6
+    L = np.linalg.cholesky(spd_batch(rng, nb, n))
+    for (oa, ob, od, reuse) in [((0, 0), (0, 0), (0, 0), False), ((3, 3), (1, 1), (1, 2), False),
+                                ((0, 0), (0, 0), (0, 0), True), ((4, 4), (2, 0), (0, 0), True)]:
+        A = rand_batch(rng, nb, oa[0] + n + 1, oa[1] + n + 2)
+        if reuse:
+            S = rand_batch(rng, nb, oa[0] + n + 1, oa[1] + n + 2)
+            S.set_window(oa[0], oa[1], spd_batch(rng, nb, n))
+            O.potrf_l(n, S, *oa, A, *oa)  # oracle factor + valid diag_inv (level3.py:169-170)
+            dA = dev(A)
+            assert dA.diag_inv_valid(oa[1], n)
+        else:
+            A.set_window(oa[0], oa[1], L)
+            dA = dev(A)
+        B = rand_batch(rng, nb, ob[0] + m, ob[1] + n + 1)
+        D = rand_batch(rng, nb, od[0] + m + 2, od[1] + n)
+        dB, dD = dev(B), dev(D)
+        info = level3.trsm_rltn(m, n, -1.5, dA.ref(*oa), dB.ref(*ob), dD.ref(*od), check=False)
+        winfo = O.trsm_rltn(m, n, -1.5, A, *oa, B, *ob, D, *od)
+        if info is not None:
+            assert np.array_equal(info.cpu().numpy(), winfo)
+        mask = np.zeros(D.per, dtype=bool)
+        for i in range(m):
+            for j in range(n):
+                mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+        compare_storage(host(dD), D.storage, mask, n, f"trsm {mn} {oa}{od} reuse={reuse}")
+
+
+def test_trsm_zero_pivot_leaves_item_untouched():
+    rng = np.random.default_rng(3)
+    for n in (4, 48, 256):
+        nb, m = 5, 7
+        L = np.linalg.cholesky(spd_batch(rng, nb, n))
+        L[2, n // 2, n // 2] = 0.0
+        A = rand_batch(rng, nb, n, n)
+        A.set_window(0, 0, L)
+        B = rand_batch(rng, nb, m, n)
+        D = rand_batch(rng, nb, m, n, fill=4.0)
+        dA, dB, dD = dev(A), dev(B), dev(D)
+        info = level3.trsm_rltn(m, n, 1.0, dA, dB, dD, check=False).cpu().numpy()
+        assert list(info) == [-1, -1, n // 2, -1, -1]
+        assert np.all(host(dD)[2] == 4.0)
+        with pytest.raises(pb.SingularMatrixError) as ei:
+            level3.trsm_rltn(m, n, 1.0, dA, dB, dD)
+        assert ei.value.index == n // 2 and ei.value.batch_index == 2
+
+
+# ---------------------------------------------------------------------------
+# discrete semantics (exact)
+
+
+def test_gemm_special_cases_exact():
+    rng = np.random.default_rng(5)
+    for (m, n, k) in [(3, 5, 7), (8, 2, 7), (40, 40, 40), (70, 66, 9)]:
+        nb = 4
+        c = rng.uniform(-1, 1, (nb, m, n))
+        dC = pack.panel_from_array(c)
+        nanA = pack.panel_from_array(np.full((nb, m, k), np.nan))
+        nanB = pack.panel_from_array(np.full((nb, n, k), np.nan))
+        dD = pb.allocate_panel_batch(nb, m, n, zero=True)
+        level3.gemm_nt(m, n, k, 0.0, nanA, nanB, 1.0, dC, dD)  # alpha=0: A*B ignored even if NaN
+        assert np.array_equal(pack.panel_to_array(dD).cpu().numpy(), c)
+        level3.gemm_nt(m, n, k, 0.0, nanA, nanB, -2.0, dC, dD)
+        assert np.array_equal(pack.panel_to_array(dD).cpu().numpy(), -2.0 * c)
+        a = pack.panel_from_array(rng.uniform(-1, 1, (nb, m, k)))
+        b = pack.panel_from_array(rng.uniform(-1, 1, (nb, n, k)))
+        nanC = pack.panel_from_array(np.full((nb, m, n), np.nan))
+        level3.gemm_nt(m, n, k, 1.0, a, b, 0.0, nanC, dD)  # beta=0: C never read
+        assert not torch.isnan(pack.panel_to_array(dD)).any()
+        level3.gemm_nt(m, n, 0, 1.0, a, b, 0.5, dC, dD)  # k=0: D = beta*C
+        assert np.array_equal(pack.panel_to_array(dD).cpu().numpy(), 0.5 * c)
+        before = dD.storage.clone()
+        level3.gemm_nt(0, n, k, 1.0, a, b, 0.0, dC, dD)  # m=0 / n=0: no-op
+        level3.gemm_nt(m, 0, k, 1.0, a, b, 0.0, dC, dD)
+        assert torch.equal(before, dD.storage)
+
+
+def test_aliasing_and_determinism_bit_exact():
+    rng = np.random.default_rng(6)
+    for (m, k) in [(9, 5), (40, 33), (96, 40)]:
+        nb = 6
+        a = pack.panel_from_array(rng.uniform(-1, 1, (nb, m, k)))
+        c = rng.uniform(-1, 1, (nb, m, m))
+        alias = pack.panel_from_array(c)
+        sep = pb.allocate_panel_batch(nb, m, m, zero=True)
+        level3.gemm_nt(m, m, k, 1.0, a, a, 0.5, alias, alias)
+        level3.gemm_nt(m, m, k, 1.0, a, a, 0.5, pack.panel_from_array(c), sep)
+        assert torch.equal(pack.panel_to_array(alias), pack.panel_to_array(sep))
+        alias = pack.panel_from_array(c)
+        sep2 = pb.allocate_panel_batch(nb, m, m, zero=True)
+        level3.syrk_ln(m, k, 1.0, a, a, 0.5, alias, alias)
+        level3.syrk_ln(m, k, 1.0, a, a, 0.5, pack.panel_from_array(c), sep2)
+        assert torch.equal(torch.tril(pack.panel_to_array(alias)), torch.tril(pack.panel_to_array(sep2)))
+        s = spd_batch(rng, nb, m)
+        inplace = pack.panel_from_array(s)
+        out = pb.allocate_panel_batch(nb, m, m, zero=True)
+        level3.potrf_l(m, inplace, inplace)
+        level3.potrf_l(m, pack.panel_from_array(s), out)
+        assert torch.equal(torch.tril(pack.panel_to_array(inplace)), torch.tril(pack.panel_to_array(out)))
+        assert torch.equal(inplace.diag_inv, out.diag_inv)
+        bm = pack.panel_from_array(rng.uniform(-1, 1, (nb, 7, m)))
+        x1 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        level3.trsm_rltn(7, m, 1.0, out, bm, x1)
+        x2 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        pack.gecp(7, m, bm, x2)
+        level3.trsm_rltn(7, m, 1.0, out, x2, x2)  # D == B in place
+        assert torch.equal(x1.storage, x2.storage)
+        # determinism: same inputs, bit-identical outputs run to run
+        x3 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        level3.trsm_rltn(7, m, 1.0, out, bm, x3)
+        assert torch.equal(x1.storage, x3.storage)
+
+
+def test_broadcast_operand():
+    rng = np.random.default_rng(11)
+    nb, m, n, k = 8, 12, 10, 9
+    a = rng.uniform(-1, 1, (nb, m, k))
+    b1 = rng.uniform(-1, 1, (1, n, k))
+    dA, dB1 = pack.panel_from_array(a), pack.panel_from_array(b1)
+    dD = pb.allocate_panel_batch(nb, m, n, zero=True)
+    level3.gemm_nt(m, n, k, 1.0, dA, dB1, 0.0, dD, dD)
+    want = a @ b1[0].T
+    assert O.rel_fro(pack.panel_to_array(dD).cpu().numpy(), want) < O.tol(k)
+
+
+# ---------------------------------------------------------------------------
+# pack / unpack / gecp: bit-exact
+
+
+def test_pack_unpack_roundtrip_bit_exact():
+    rng = np.random.default_rng(2)
+    for trial in range(60):
+        nb = int(rng.integers(1, 6))
+        m, n = int(rng.integers(0, 40)), int(rng.integers(0, 40))
+        ai, aj = int(rng.integers(0, 9)), int(rng.integers(0, 9))
+        arr = rng.uniform(-1, 1, (nb, m, n))
+        big = pb.allocate_panel_batch(nb, ai + m + 3, aj + n + 3, zero=True)
+        src = pack.ColBatch.from_array(arr)
+        pack.pack_matrix(src, m, n, big.ref(ai, aj))
+        out = pack.ColBatch.from_array(np.zeros((nb, m, n)))
+        pack.unpack_matrix(big.ref(ai, aj), m, n, out)
+        assert np.array_equal(out.to_array().cpu().numpy(), arr), (m, n, ai, aj)
+        # panel bytes equal the oracle's kpack_cm (and padding untouched)
+        h = O.HostBatch(nb, ai + m + 3, aj + n + 3)
+        cm = np.ascontiguousarray(arr.transpose(0, 2, 1)).reshape(nb, -1)
+        if m * n:
+            O.pack_cm(m, n, cm.reshape(-1), max(m, 1), m * n, h, ai, aj)
+        assert np.array_equal(host(big).view(np.uint64), h.storage.view(np.uint64))
+        # row-major bridges
+        back = pack.panel_to_array(big.ref(ai, aj), m, n).cpu().numpy()
+        assert np.array_equal(back, arr)
+        big2 = pb.allocate_panel_batch(nb, ai + m + 3, aj + n + 3, zero=True)
+        pack.gecp(m, n, big.ref(ai, aj), big2.ref(ai, aj))
+        assert torch.equal(big.storage, big2.storage)
+
+
+def test_pack_kat_element_46():
+    d = pb.allocate_panel_batch(2, 8, 8, zero=True)
+    pack.pack_matrix(pack.ColBatch.from_array(np.full((2, 1, 1), 5.0)), 1, 1, d.ref(6, 3))
+    assert torch.all(d.data[:, 46] == 5.0) and float(d.data.abs().sum()) == 20.0
+
+
+# ---------------------------------------------------------------------------
+# BASELINE-size batches: sampled oracle + size-independent properties
+
+
+def test_config1_full_batch_sampled():
+    """C1: gemm_nt 64^3, alpha=beta=1, batch 4096 (BASELINE configs[0])."""
+    nb, s = 4096, 64
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A, B, C = (pb.allocate_panel_batch(nb, s, s) for _ in range(3))
+    for x in (A, B, C):
+        x.storage.uniform_(-1, 1, generator=g)
+    D = pb.allocate_panel_batch(nb, s, s, zero=True)
+    level3.gemm_nt(s, s, s, 1.0, A, B, 1.0, C, D)
+    # linearity: gemm(2A) - 2 gemm(A) with beta=0 is exactly zero
+    D2 = pb.allocate_panel_batch(nb, s, s, zero=True)
+    A2 = pb.create_panel_batch(nb, s, s, A.storage * 2.0)
+    level3.gemm_nt(s, s, s, 1.0, A2, B, 0.0, C, D2)
+    D1 = pb.allocate_panel_batch(nb, s, s, zero=True)
+    level3.gemm_nt(s, s, s, 1.0, A, B, 0.0, C, D1)
+    assert torch.equal(D2.data, 2.0 * D1.data)
+    idx = np.random.default_rng(0).choice(nb, 12, replace=False)
+    sub = torch.as_tensor(idx, device="cuda")
+    hA, hB, hC = (O.HostBatch(12, s, s, x.storage[sub].cpu().numpy()) for x in (A, B, C))
+    hD = O.HostBatch(12, s, s)
+    O.gemm_nt(s, s, s, 1.0, hA, 0, 0, hB, 0, 0, 1.0, hC, 0, 0, hD, 0, 0)
+    fp_close(D.data[sub].cpu().numpy(), hD.storage[:, : 64 * 64], s, "C1 sample")
+
+
+@pytest.mark.parametrize("n", [4, 16, 64, 256])
+def test_config2_potrf_large_batch_residual(n):
+    """C2: potrf at large batch: residual ||L L^T - A|| / ||A|| and sampled oracle."""
+    nb = {4: 1 << 20, 16: 1 << 16, 64: 8192, 256: 256}[n]
+    g = torch.Generator(device="cuda").manual_seed(n)
+    M = torch.rand((nb, n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = M @ M.transpose(1, 2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    C = pack.panel_from_array(a)
+    D = pb.allocate_panel_batch(nb, n, n, zero=True)
+    info = level3.potrf_l(n, C, D)
+    assert int((info >= 0).sum()) == 0
+    L = torch.tril(pack.panel_to_array(D))
+    res = torch.linalg.matrix_norm(L @ L.transpose(1, 2) - a) / torch.linalg.matrix_norm(a)
+    assert float(res.max()) <= 50 * n * EPS
+    dinv = D.diag_inv
+    assert float((dinv * torch.diagonal(L, dim1=1, dim2=2) - 1).abs().max()) <= 4 * EPS
+    idx = torch.as_tensor(np.random.default_rng(n).choice(nb, 8, replace=False), device="cuda")
+    hC = O.HostBatch(8, n, n, C.storage[idx].cpu().numpy())
+    hD = O.HostBatch(8, n, n)
+    O.potrf_l(n, hC, 0, 0, hD, 0, 0)
+    fp_close(torch.tril(L[idx]).cpu().numpy(), np.tril(hD.window(0, 0, n, n)), n, "C2 sample")

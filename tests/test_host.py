@@ -1,0 +1,130 @@
+"""CPU: host-side logic of the product package and the C-ABI boundary.
+
+No CUDA device is needed: these cover the storage layer (reference KATs),
+argument validation (DimensionError before any launch, reference
+messages), and that libpb_b200.so loads and exports every entry point
+include/pb_b200.h declares.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import REPO
+import paper_1704_02457_b200 as pb
+from paper_1704_02457_b200 import _native, level3, pack
+from paper_1704_02457_b200.matstore import element_offset, memsize_panel_matrix
+
+
+def test_element_offset_and_memsize_kats():
+    # reference tests/test_matstore.py:14-17, 42-47
+    assert element_offset(6, 3, 4, 8) == 46
+    assert element_offset(4, 0, 4, 8) == 32
+    assert memsize_panel_matrix(4, 4) == 192
+    assert memsize_panel_matrix(5, 3) == 320
+    assert memsize_panel_matrix(64, 64) == 33280  # C1 item
+
+
+def test_element_offset_injective_in_bounds():
+    for m in range(1, 21):
+        for n in range(1, 21):
+            cn = -(-n // 4) * 4
+            offs = {element_offset(i, j, 4, cn) for i in range(m) for j in range(n)}
+            assert len(offs) == m * n
+            assert max(offs) < -(-m // 4) * 4 * cn
+
+
+def test_panel_batch_views_on_cpu_storage():
+    nb, m, n = 3, 6, 5
+    p = pb.allocate_panel_batch(nb, m, n, device="cpu", zero=True)
+    assert p.storage.shape == (nb, memsize_panel_matrix(m, n) // 8)
+    assert p.data.shape == (nb, 8 * 8)
+    assert p.diag_inv.shape == (nb, 5)
+    assert p.panels().shape == (nb, 2, 8, 4)
+    p.panels()[1, 1, 3, 2] = 7.0  # row 6, col 3
+    assert float(p.data[1, element_offset(6, 3, 4, 8)]) == 7.0
+    d = p.descriptor()
+    assert (d.m, d.n, d.cn, d.batch, d.stride) == (m, n, 8, nb, p.storage.shape[1])
+    assert d.dA - d.pA == 64 * 8
+    one = pb.allocate_panel_batch(1, m, n, device="cpu")
+    bd = one.descriptor(7)
+    assert bd.batch == 7 and bd.stride == 0
+    with pytest.raises(pb.DimensionError):
+        p.descriptor(7)
+
+
+def test_create_panel_batch_validation():
+    with pytest.raises(pb.MemoryLayoutError, match="required"):
+        pb.create_panel_batch(2, 4, 4, torch.zeros(40, dtype=torch.float64))
+    buf = torch.zeros(100, dtype=torch.float64)
+    q = pb.create_panel_batch(2, 4, 4, buf)
+    assert q.storage.data_ptr() == buf.data_ptr()  # no copy, contents untouched
+    with pytest.raises(pb.MemoryLayoutError):
+        pb.create_panel_batch(1, 4, 4, torch.zeros(100, dtype=torch.float32))
+
+
+def test_level3_bounds_errors_before_launch():
+    a = pb.allocate_panel_batch(2, 4, 4, device="cpu")
+    with pytest.raises(pb.DimensionError, match="A window"):
+        level3.gemm_nt(5, 4, 4, 1.0, a, a, 0.0, a, a)
+    with pytest.raises(pb.DimensionError, match="negative"):
+        level3.gemm_nt(-1, 4, 4, 1.0, a, a, 0.0, a, a)
+    with pytest.raises(pb.DimensionError):
+        level3.syrk_ln(4, 5, 1.0, a, a, 0.0, a, a)
+    with pytest.raises(pb.DimensionError):
+        level3.trsm_rltn(4, 5, 1.0, a, a, a)
+    with pytest.raises(pb.DimensionError):
+        level3.potrf_l(3, a, a, n=5)
+    with pytest.raises(pb.DimensionError):
+        pb.SubRef(a, -1, 0)
+    with pytest.raises(ValueError, match="variant"):
+        level3.trsm(2, 2, 1.0, a, a, a, "rltx")
+    with pytest.raises(NotImplementedError):
+        level3.trsm(2, 2, 1.0, a, a, a, "llnu")
+    # valid windows on CPU storage: refuses loudly (no CPU fallback)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        level3.gemm_nt(4, 4, 4, 1.0, a, a, 0.0, a, a)
+
+
+def _header_symbols():
+    text = open(os.path.join(REPO, "include", "pb_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*|int64_t)\s*(pb_\w+)\(", text, re.M)))
+
+
+def test_native_library_exports_header_surface():
+    lib = _native.load()
+    syms = _header_symbols()
+    assert len(syms) == 12, syms
+    assert set(syms) == set(_native.SIGNATURES)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.pb_version() == 1
+    # argument validation needs no device: a bad size returns -position
+    d = pb.allocate_panel_batch(1, 4, 4, device="cpu").descriptor()
+    assert lib.pb_dgemm_nt(-1, 4, 4, 1.0, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, 0.0, ctypes.byref(d), 0, 0,
+                           ctypes.byref(d), 0, 0, None) == -1
+    assert b"negative" in lib.pb_last_error()
+    assert lib.pb_dpotrf_l(4, 5, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, None, None) == -2
+    assert lib.pb_dgemm_nt(4, 4, 4, 1.0, ctypes.byref(d), 1, 0, ctypes.byref(d), 0, 0, 0.0, ctypes.byref(d), 0, 0,
+                           ctypes.byref(d), 0, 0, None) == -5
+    assert lib.pb_launch_count(0) == 0
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(REPO, "paper_1704_02457_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(root, f)).read()
+                assert "oracle" not in txt.replace("oracle's", ""), f
+
+
+def test_colbatch_roundtrip_host_side():
+    arr = np.arange(2 * 3 * 4, dtype=np.float64).reshape(2, 3, 4)
+    cb = pack.ColBatch.from_array(arr, device="cpu")
+    assert cb.lda == 3 and cb.data.shape == (2, 12)
+    assert float(cb.data[1, 0 + 2 * 3]) == arr[1, 0, 2]
+    assert np.array_equal(cb.to_array().numpy(), arr)

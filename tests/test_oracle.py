@@ -1,0 +1,157 @@
+"""CPU: pin the oracle (oracle/pb_oracle.c) to the reference.
+
+1. Bit-exact reproduction of every golden case recorded from the
+   reference's own public API (tests/golden/make_golden.py).
+2. Bit-exact agreement with the reference's compiled core itself
+   (oracle/_ref, cythonized from ccore.pyx) on random panel data, when
+   that build is present (it is built in the build container only).
+3. The reference's known-answer tests for the layout (matstore KATs).
+"""
+import glob
+import importlib.util
+import os
+
+import numpy as np
+import pytest
+
+from conftest import REPO, load_golden
+from golden_util import host_inputs, out_labels, run_oracle
+from oracle import oracle as O
+
+
+def test_layout_kats():
+    # tests/test_matstore.py:14-17, 42-47 of the reference
+    lib = O.lib()
+    assert lib.po_element_offset(6, 3, 8) == 46
+    assert lib.po_element_offset(4, 0, 8) == 32
+    assert lib.po_memsize(4, 4) == 192
+    assert lib.po_memsize(5, 3) == 320
+    assert O.memsize(4, 4) == 192 and O.memsize(5, 3) == 320
+
+
+def test_golden_cases_bit_exact():
+    z, cases = load_golden()
+    assert len(cases) >= 70
+    for case in cases:
+        mats = host_inputs(z, case)
+        st = run_oracle(case, mats, z)
+        assert st == case["status"], (case["name"], st, case["status"])
+        for lab in out_labels(case):
+            want = z[f"{case['key']}/out/{lab}"]
+            got = mats[lab].storage[0, : want.size]
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (case["name"], lab)
+        if case["op"] == "potrf_l":
+            d = mats[case["alias"].get("D", "D")]
+            assert [d.diag_lo, d.diag_hi] == case["valid_out"]["D"], case["name"]
+
+
+def _load_ref_core():
+    so = glob.glob(os.path.join(REPO, "oracle", "_ref", "ccore*.so"))
+    if not so:
+        return None
+    spec = importlib.util.spec_from_file_location("ccore", so[0])
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+ref_core = _load_ref_core()
+
+
+@pytest.mark.skipif(ref_core is None, reason="oracle/_ref not built (make -C oracle ref)")
+def test_oracle_matches_compiled_reference_core():
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        m, n, k = (int(x) for x in rng.integers(1, 40, 3))
+        sd_a, sd_b, sd_c, sd_d = (int(x) * 4 + 4 * ((k + 3) // 4 + 3) for x in rng.integers(1, 4, 4))
+        sd_c = sd_d = max(sd_c, 4 * ((n + 3) // 4) + 8)
+        rows = 4 * ((m + 3) // 4) + 8
+        A = rng.standard_normal(rows * sd_a)
+        B = rng.standard_normal((4 * ((n + 3) // 4) + 8) * sd_b)
+        C = rng.standard_normal(rows * sd_c)
+        D1 = rng.standard_normal(rows * sd_d)
+        D2 = D1.copy()
+        ci, cj, di = int(rng.integers(0, 4)), int(rng.integers(0, 3)), int(rng.integers(0, 4))
+        alpha, beta = float(rng.choice([1.0, -1.5, 0.0])), float(rng.choice([0.0, 0.5, 1.0]))
+        ref_core.gemm_nt_drv(m, n, k, alpha, A, 0, 1, sd_a, B, 4, 2, sd_b, beta, C, ci, cj, sd_c, D1, di, 1, sd_d)
+        O.lib().po_gemm_nt(*[O._L(x) for x in (m, n, k)], O._D(alpha),
+                           A.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(1), O._L(sd_a),
+                           B.ctypes.data_as(O.ctypes.c_void_p), O._L(4), O._L(2), O._L(sd_b), O._D(beta),
+                           C.ctypes.data_as(O.ctypes.c_void_p), O._L(ci), O._L(cj), O._L(sd_c),
+                           D2.ctypes.data_as(O.ctypes.c_void_p), O._L(di), O._L(1), O._L(sd_d))
+        assert np.array_equal(D1.view(np.uint64), D2.view(np.uint64)), ("gemm", trial)
+        # syrk (square m), shared A/B stream at an aligned row
+        sd_s = 4 * ((m + 3) // 4) + 8
+        C = rng.standard_normal(rows * sd_s)
+        S1 = rng.standard_normal(rows * sd_s)
+        S2 = S1.copy()
+        sd_c = sd_d = sd_s
+        ref_core.syrk_ln_drv(m, k, alpha, A, 4, 0, sd_a, A, 4, 0, sd_a, beta, C, ci, 0, sd_c, S1, di, 0, sd_d)
+        O.lib().po_syrk_ln(O._L(m), O._L(k), O._D(alpha),
+                           A.ctypes.data_as(O.ctypes.c_void_p), O._L(4), O._L(0), O._L(sd_a),
+                           A.ctypes.data_as(O.ctypes.c_void_p), O._L(4), O._L(0), O._L(sd_a), O._D(beta),
+                           C.ctypes.data_as(O.ctypes.c_void_p), O._L(ci), O._L(0), O._L(sd_c),
+                           S2.ctypes.data_as(O.ctypes.c_void_p), O._L(di), O._L(0), O._L(sd_d))
+        assert np.array_equal(S1.view(np.uint64), S2.view(np.uint64)), ("syrk", trial)
+
+
+@pytest.mark.skipif(ref_core is None, reason="oracle/_ref not built (make -C oracle ref)")
+def test_oracle_factorizations_match_compiled_reference_core():
+    rng = np.random.default_rng(8)
+    for trial in range(30):
+        n = int(rng.integers(1, 45))
+        m = n + int(rng.integers(0, 9))
+        sd = 4 * ((n + 3) // 4)
+        rows = 4 * ((m + 3) // 4)
+        g = rng.uniform(-1, 1, (m, n))
+        full = np.zeros((m, n))
+        full[:n] = g[:n] @ g[:n].T + n * np.eye(n)
+        full[n:] = g[n:]
+        if trial % 5 == 4:
+            f = int(rng.integers(0, n))
+            full[f, f] = -1.0
+        C = np.zeros(rows * sd)
+        for i in range(m):
+            for j in range(n):
+                C[O.element_offset(i, j, sd)] = full[i, j]
+        D1 = np.full(rows * sd, 7.0)
+        D2 = D1.copy()
+        v1 = np.zeros(n)
+        v2 = np.zeros(n)
+        st1 = ref_core.potrf_drv(m, n, C, 0, 0, sd, D1, 0, 0, sd, v1, 0)
+        st2 = O.lib().po_potrf_l(O._L(m), O._L(n), C.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(0), O._L(sd),
+                                 D2.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(0), O._L(sd),
+                                 v2.ctypes.data_as(O.ctypes.c_void_p), O._L(0))
+        assert st1 == st2, trial
+        assert np.array_equal(D1.view(np.uint64), D2.view(np.uint64)), ("potrf", trial)
+        assert np.array_equal(v1.view(np.uint64), v2.view(np.uint64)), ("dinv", trial)
+        if st1 >= 0:
+            continue
+        # trsm_rltn against the fresh factor, reusing its reciprocals
+        mm = int(rng.integers(1, 30))
+        rows_b = 4 * ((mm + 3) // 4)
+        B = rng.uniform(-1, 1, rows_b * sd)
+        X1 = np.zeros(rows_b * sd)
+        X2 = X1.copy()
+        ref_core.trsm_rltn_drv(mm, n, 1.5, D1, 0, 0, sd, False, B, 0, 0, sd, X1, 0, 0, sd, v1, 0)
+        O.lib().po_trsm_rltn(O._L(mm), O._L(n), O._D(1.5), D2.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(0),
+                             O._L(sd), O.ctypes.c_int(0), B.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(0),
+                             O._L(sd), X2.ctypes.data_as(O.ctypes.c_void_p), O._L(0), O._L(0), O._L(sd),
+                             v2.ctypes.data_as(O.ctypes.c_void_p), O._L(0))
+        assert np.array_equal(X1.view(np.uint64), X2.view(np.uint64)), ("trsm", trial)
+
+
+def test_oracle_potrf_against_numpy():
+    rng = np.random.default_rng(9)
+    for n in (1, 3, 8, 17, 40):
+        g = rng.uniform(-1, 1, (n, n))
+        a = g @ g.T + n * np.eye(n)
+        C = O.HostBatch(1, n, n)
+        C.set_window(0, 0, a[None])
+        D = O.HostBatch(1, n, n)
+        info = O.potrf_l(n, C, 0, 0, D, 0, 0)
+        assert info[0] == -1
+        got = np.tril(D.window(0, 0, n, n)[0])
+        assert O.rel_fro(got, np.linalg.cholesky(a)) < O.tol(n)
+        dinv = D.storage[0, D.diag_off: D.diag_off + n]
+        assert np.max(np.abs(dinv * np.diag(got) - 1.0)) <= 1e-15  # tests/test_acceptance.py:266-267
