@@ -339,6 +339,7 @@ bool potrf_fits(ix m, ix n) {
 }
 
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
+  if (potrf_small_ok(g)) return run_potrf_small(g, st);
   const ix gm = (g.m + 7) / 8;
   if (gm <= 2) return launch_potrf<1, 2>(g, st);
   if (gm <= 4) return launch_potrf<1, 4>(g, st);

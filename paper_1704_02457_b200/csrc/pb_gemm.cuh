@@ -61,6 +61,8 @@ cudaError_t run_unpack(const CopyArgs &g, cudaStream_t st);
 cudaError_t run_gecp(const CopyArgs &g, cudaStream_t st);
 cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *info, cudaStream_t st);
 bool potrf_fits(ix m, ix n);
+bool potrf_small_ok(const PotrfArgs &g);
+cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
 
 }  // namespace pb

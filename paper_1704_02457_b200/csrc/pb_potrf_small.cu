@@ -1,0 +1,398 @@
+// Batched dpotrf_l for tiny matrices (n <= 16): register-resident,
+// bit-exact with the reference (sm_100a).
+//
+// For n <= 16 the factorization is pure HBM streaming (AI < 0.6 flop/B),
+// so the kernel is built around the memory system:
+//  * persistent CTAs, double-buffered: while a round of items is factored
+//    from shared memory, the next round's lower-triangle panel prefixes
+//    stream in with 16-byte cp.async (one panel row-block of the lower
+//    triangle, columns [0, 4p+4), is a contiguous run in panel-major);
+//  * every lane of a warp issues consecutive 16-byte pieces, so loads and
+//    the masked stores of the results are fully coalesced;
+//  * n <= 8: one thread owns one item, entirely in registers;
+//    9 <= n <= 16: a quad of threads owns one item, thread q owning panel q
+//    (rows 4q..4q+3), left-looking over 4-column blocks with the block row
+//    broadcast through warp shuffles.
+//
+// Arithmetic follows the reference's per-element operation order exactly
+// (potrf_drv ccore.pyx:877-905, _kpotrf_core :404-438, _trsm_rltn_core
+// :358-388): downdate sum from 0.0 over l ascending, then + C, then the
+// in-tile updates, IEEE sqrt and division, no FMA contraction -- so the
+// factor and diag_inv are bit-identical to the reference's.  Failure
+// index and the partially written factor of a failing item match too.
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+template <int N>
+struct SmallCfg {
+  static constexpr int NP = (N + 3) / 4;  // panels
+  static constexpr int T = N <= 8 ? 1 : 4;  // threads per item
+  static constexpr int NTHREADS = 128;
+  static constexpr int ITEMS = NTHREADS / T;
+  __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
+  __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
+  static constexpr int ITEM_ELEMS = poff(NP);        // lower-prefix doubles per item
+  static constexpr int STRIDE = ITEM_ELEMS + 2;      // padded (keeps 16-byte alignment)
+  static constexpr int BUF = ITEMS * STRIDE;
+  static constexpr int DINV = ITEMS * N;  // one round's reciprocals
+  static constexpr size_t SMEM = sizeof(double) * (2 * BUF + DINV) + sizeof(int) * ITEMS;
+};
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// One item, one thread (n <= 8).  L holds C's lower prefix on entry (rows
+// 0..4NP-1, cols 0..N-1 as available) and the factor on exit.
+template <int N>
+__device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], double *dinv) {
+  constexpr int NP = SmallCfg<N>::NP;
+#pragma unroll
+  for (int ii = 0; ii < NP; ++ii) {
+    constexpr int dummy = 0;
+    (void)dummy;
+#pragma unroll
+    for (int jj = 0; jj <= ii; ++jj) {
+      const int ns = N - 4 * jj < 4 ? N - 4 * jj : 4;
+      double acc[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double s = 0.0;
+#pragma unroll
+          for (int l = 0; l < 4 * jj; ++l)
+            if (c < ns) s = dadd(s, dmul(L[4 * ii + r][l], -L[4 * jj + c][l]));
+          acc[c][r] = s;
+        }
+      if (jj < ii) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < ns) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[c][r] = dadd(acc[c][r], L[4 * ii + r][4 * jj + c]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (t < c) {
+                const double e = L[4 * jj + c][4 * jj + t];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[c][r] = dsub(acc[c][r], dmul(acc[t][r], e));
+              }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              acc[c][r] = dmul(acc[c][r], dinv[4 * jj + c]);
+              L[4 * ii + r][4 * jj + c] = acc[c][r];
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (c < ns) acc[c][r] = dadd(acc[c][r], L[4 * ii + r][4 * jj + c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < ns) {
+            const double d = acc[c][c];
+            if (d <= 0.0) return 4 * jj + c;
+            const double ljj = __dsqrt_rn(d);
+            const double inv = __ddiv_rn(1.0, ljj);
+            acc[c][c] = ljj;
+            dinv[4 * jj + c] = inv;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              if (r > c) acc[c][r] = dmul(acc[c][r], inv);
+#pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2)
+              if (c2 > c && c2 < ns) {
+                const double lcj = acc[c][c2];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                  if (r >= c2) acc[c2][r] = dsub(acc[c2][r], dmul(acc[c][r], lcj));
+              }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (c < ns && r >= c) L[4 * ii + r][4 * jj + c] = acc[c][r];
+      }
+    }
+  }
+  return -1;
+}
+
+// One item, a quad of threads (9 <= n <= 16): thread q owns panel q.
+// Left-looking over column blocks s; per element the operation order is
+// the reference's (see file header), so results are bit-identical.  The
+// quad stays converged around every shuffle; only the diagonal factor
+// (no shuffles) runs on thread s alone.
+template <int N>
+__device__ __forceinline__ int factor_t4(double (&L)[4][N], double *dinv, int q, int qbase) {
+  constexpr int NP = SmallCfg<N>::NP;
+  int fail = -1;
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    const int ns = N - 4 * s < 4 ? N - 4 * s : 4;
+    const bool alive = fail < 0;
+    double acc[4][4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[c][r] = 0.0;
+    // downdate with block row s (broadcast from thread s), l ascending
+#pragma unroll
+    for (int l = 0; l < 4 * s; ++l) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < ns) {
+          const double v = __shfl_sync(0xffffffffu, L[c][l], qbase + s);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[c][r] = dadd(acc[c][r], dmul(L[r][l], -v));
+        }
+      }
+    }
+    // + C (still held in L for column block s)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (c < ns) acc[c][r] = dadd(acc[c][r], L[r][4 * s + c]);
+    int f = -1;
+    if (q == s && alive) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < ns && f < 0) {
+          const double d = acc[c][c];
+          if (d <= 0.0) {
+            f = c;
+          } else {
+            const double ljj = __dsqrt_rn(d);
+            const double inv = __ddiv_rn(1.0, ljj);
+            acc[c][c] = ljj;
+            dinv[4 * s + c] = inv;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              if (r > c) acc[c][r] = dmul(acc[c][r], inv);
+#pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2)
+              if (c2 > c && c2 < ns) {
+                const double lcj = acc[c][c2];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                  if (r >= c2) acc[c2][r] = dsub(acc[c2][r], dmul(acc[c][r], lcj));
+              }
+          }
+        }
+      }
+    }
+    const int fs = __shfl_sync(0xffffffffu, f, qbase + s);
+    if (alive && fs >= 0) fail = 4 * s + fs;
+    // the diagonal block's factor (strictly lower part) and reciprocals
+    double E[4][4], iv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      iv[c] = c < ns ? __shfl_sync(0xffffffffu, acc[c][c], qbase + s) : 1.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) E[c][t] = (t < c && c < ns) ? __shfl_sync(0xffffffffu, acc[t][c], qbase + s) : 0.0;
+    }
+    if (q > s && fail < 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < ns) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < c) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) acc[c][r] = dsub(acc[c][r], dmul(acc[t][r], E[c][t]));
+            }
+          // reciprocal = 1/L[c][c] exactly as the factor stored it
+          const double inv = __ddiv_rn(1.0, iv[c]);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[c][r] = dmul(acc[c][r], inv);
+        }
+      }
+    }
+    if ((q >= s) && alive) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (c < ns) L[r][4 * s + c] = acc[c][r];
+    }
+  }
+  return fail;
+}
+
+template <int N>
+__global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(PotrfArgs g) {
+  using Cfg = SmallCfg<N>;
+  constexpr int NP = Cfg::NP, T = Cfg::T, ITEMS = Cfg::ITEMS, STRIDE = Cfg::STRIDE, NTH = Cfg::NTHREADS;
+  extern __shared__ __align__(128) double smem[];
+  double *sdinv = smem + 2 * Cfg::BUF;
+  int *sinfo = (int *)(sdinv + Cfg::DINV);
+  const int tid = threadIdx.x;
+  const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
+  const double *Cb = g.C.p;
+  double *Db = g.D.p;
+
+  // stage the lower prefix of round `rd`'s items into buffer `buf`: panel p
+  // of an item contributes columns [0, cols(p)) = 2*cols(p) 16-byte pieces
+  auto issue = [&](ix rd, int buf) {
+    double *S = smem + buf * Cfg::BUF;
+    const ix b0 = rd * ITEMS;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int pieces = 2 * Cfg::cols(p);
+      for (int q = tid; q < ITEMS * pieces; q += NTH) {
+        const int it = q / pieces, w = q - it * pieces;
+        const int col = w >> 1, h = w & 1;
+        const ix b = b0 + it;
+        const bool ok = b < g.batch;
+        const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
+        cp_async16(S + it * STRIDE + Cfg::poff(p) + 4 * col + 2 * h, src, ok ? 16 : 0);
+      }
+    }
+  };
+
+  if (blockIdx.x < nrounds) issue(blockIdx.x, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf ^= 1) {
+    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double *S = smem + buf * Cfg::BUF;
+    const int it = tid / T, q = tid % T;
+    double *Si = S + it * STRIDE;
+    double *di = sdinv + it * N;
+    int fail;
+    if constexpr (T == 1) {
+      double L[4 * NP][N];
+#pragma unroll
+      for (int r = 0; r < 4 * NP; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) L[r][c] = c < Cfg::cols(r >> 2) ? Si[Cfg::poff(r >> 2) + 4 * c + (r & 3)] : 0.0;
+      fail = factor_t1<N>(L, di);
+#pragma unroll
+      for (int r = 0; r < 4 * NP; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          if (c < Cfg::cols(r >> 2)) Si[Cfg::poff(r >> 2) + 4 * c + (r & 3)] = L[r][c];
+    } else {
+      double L[4][N];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) L[r][c] = 0.0;
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (p == q) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < N; ++c)
+              if (c < Cfg::cols(p)) L[r][c] = Si[Cfg::poff(p) + 4 * c + r];
+        }
+      fail = factor_t4<N>(L, di, q, (tid & 31) & ~(T - 1));
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (p == q) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < N; ++c)
+              if (c < Cfg::cols(p)) Si[Cfg::poff(p) + 4 * c + r] = L[r][c];
+        }
+    }
+    const ix b0 = rd * ITEMS;
+    if (q == 0) {
+      sinfo[it] = fail;
+      if (b0 + it < g.batch && g.info) g.info[b0 + it] = fail;
+    }
+    __syncthreads();
+    // masked, coalesced stores of the lower triangle (the reference's write set)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int pieces = 2 * Cfg::cols(p);
+      for (int qq = tid; qq < ITEMS * pieces; qq += NTH) {
+        const int it2 = qq / pieces, w = qq - it2 * pieces;
+        const int col = w >> 1, h = w & 1;
+        const ix bb = b0 + it2;
+        if (bb >= g.batch) continue;
+        const int f = sinfo[it2];
+        const int r0 = 4 * p + 2 * h;
+        bool w0 = r0 >= col && r0 < N, w1 = r0 + 1 >= col && r0 + 1 < N;
+        if (f >= 0) {
+          const int iif = f & ~3;
+          w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
+          w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+        }
+        const double *src = S + it2 * STRIDE + Cfg::poff(p) + 4 * col + 2 * h;
+        double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+        if (w0 && w1) {
+          *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(src);
+        } else if (w0) {
+          dst[0] = src[0];
+        } else if (w1) {
+          dst[1] = src[1];
+        }
+      }
+    }
+    // reciprocals: dA[dj + c] for c < (fail >= 0 ? fail : n)
+    for (int qq = tid; qq < ITEMS * N; qq += NTH) {
+      const int it2 = qq / N, c = qq - it2 * N;
+      const ix bb = b0 + it2;
+      const int f = sinfo[it2];
+      if (bb < g.batch && (f < 0 || c < f)) g.D.d[bb * g.D.dstride + g.dj + c] = sdinv[qq];
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+template <int N>
+static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
+  using Cfg = SmallCfg<N>;
+  auto kern = potrf_small_kernel<N>;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > rounds) grid = rounds;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, Cfg::NTHREADS, Cfg::SMEM, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
+bool potrf_small_ok(const PotrfArgs &g) {
+  if (g.m != g.n || g.n > 16 || g.n < 1 || g.merge) return false;
+  if ((g.ci & 3) || (g.di & 3)) return false;
+  if (((uintptr_t)g.C.p & 15) || ((uintptr_t)g.D.p & 15)) return false;
+  if ((g.C.stride & 1) || (g.D.stride & 1)) return false;
+  return true;
+}
+
+cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
+  switch (g.n) {
+#define PB_SMALL(N_) \
+  case N_:           \
+    return launch_small<N_>(g, st);
+    PB_SMALL(1) PB_SMALL(2) PB_SMALL(3) PB_SMALL(4) PB_SMALL(5) PB_SMALL(6) PB_SMALL(7) PB_SMALL(8)
+    PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15) PB_SMALL(16)
+#undef PB_SMALL
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pb

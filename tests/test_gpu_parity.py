@@ -407,7 +407,7 @@ def test_pack_unpack_roundtrip_bit_exact():
 def test_pack_kat_element_46():
     d = pb.allocate_panel_batch(2, 8, 8, zero=True)
     pack.pack_matrix(pack.ColBatch.from_array(np.full((2, 1, 1), 5.0)), 1, 1, d.ref(6, 3))
-    assert torch.all(d.data[:, 46] == 5.0) and float(d.data.abs().sum()) == 20.0
+    assert torch.all(d.data[:, 46] == 5.0) and float(d.data.abs().sum()) == 10.0
 
 
 # ---------------------------------------------------------------------------
@@ -459,3 +459,24 @@ def test_config2_potrf_large_batch_residual(n):
     hD = O.HostBatch(8, n, n)
     O.potrf_l(n, hC, 0, 0, hD, 0, 0)
     fp_close(torch.tril(L[idx]).cpu().numpy(), np.tril(hD.window(0, 0, n, n)), n, "C2 sample")
+
+
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_potrf_small_bit_exact(n):
+    """n <= 16 runs the register kernel that follows the reference's operation
+    order exactly: factor and diag_inv are bit-identical to the oracle (and so
+    to the reference's compiled core), including failing items."""
+    rng = np.random.default_rng(100 + n)
+    nb = 300
+    a = spd_batch(rng, nb, n)
+    for b in range(0, nb, 7):
+        f = int(rng.integers(0, n))
+        a[b, f, f] = -1.0 - 10.0 * n
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    D = rand_batch(rng, nb, n, n, fill=-3.25)
+    dC, dD = dev(C), dev(D)
+    info = level3.potrf_l(n, dC, dD, check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
+    assert np.array_equal(info, winfo)
+    assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64))
