@@ -85,8 +85,8 @@ __device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double
       if (d <= 0.0) {
         fail = c;
       } else {
-        const double ljj = sqrt(d);
-        const double inv = 1.0 / ljj;
+        const double inv = rsqrt(d);  // 1/L[c,c] (<= 1 ulp), one MUFU + Newton
+        const double ljj = d * inv;
         if (fc == (c >> 1)) {
           if (fr == c) x[c & 1] = ljj;
           else if (fr > c) x[c & 1] = __dmul_rn(x[c & 1], inv);
@@ -106,8 +106,36 @@ __device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double
 // ---------------------------------------------------------------------------
 // potrf team kernel
 
-template <int TW, int MAXT>
-__global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems) {
+// Stage item b's lower trapezoid of C into the tri layout.  vec: 16-byte
+// cp.async pieces (panel-aligned window, asynchronous); else 8-byte loads.
+// Columns >= n and panels past m are zero-filled; upper elements inside a
+// diagonal tile are loaded as-is (never used for the lower factor).
+__device__ __forceinline__ void tri_load(double *S, const Tri &t, const double *C, ix cn, ix ci, ix cj, int m, int n,
+                                         int gm, bool vec, int ttid, int tthreads) {
+  for (int gg = 0; gg < gm; ++gg) {
+    const int w = t.width(gg), base = t.group_off(gg);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int r0 = 8 * gg + 4 * half;
+      if (vec) {
+        for (int q = ttid; q < 2 * w; q += tthreads) {
+          const int c = q >> 1, h2 = q & 1;
+          const bool ok = r0 < m && c < n;
+          const double *src = ok ? C + eo(ci + r0, cj + c, cn) + 2 * h2 : C;
+          cp_async16(S + base + half * 4 * w + 4 * c + 2 * h2, src, ok ? 16 : 0);
+        }
+      } else {
+        for (int q = ttid; q < 4 * w; q += tthreads) {
+          const int c = q >> 2, r = r0 + (q & 3);
+          S[base + half * 4 * w + q] = (r < m && c < n && c <= r) ? C[eo(ci + r, cj + c, cn)] : 0.0;
+        }
+      }
+    }
+  }
+}
+
+template <int TW, int MAXT, bool DB>
+__global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int team = warp / TW, tw = warp % TW;
@@ -120,25 +148,31 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   t.gn = t.cn8 / 8;
   const int gm = (m + 7) / 8;
   const int tri_elems = (int)Tri::size(m, n);
-  double *S = smem + (ix)team * team_elems;
-  double *dinv = S + tri_elems;                        // cn8 doubles
+  double *S0 = smem + (ix)team * team_elems;
+  double *S1 = DB ? S0 + tri_elems : S0;
+  double *dinv = S0 + (DB ? 2 : 1) * tri_elems;         // cn8 doubles
   volatile int *flag = (volatile int *)(dinv + t.cn8);  // failure index
   const int fr = lane >> 2, fc = lane & 3;
   const bool aligned_out = (g.di & 3) == 0;
+  const bool vin = vec_in != 0;
+  const ix stride = (ix)gridDim.x * teams_per_cta;
 
-  for (ix b = (ix)blockIdx.x * teams_per_cta + team; b < g.batch; b += (ix)gridDim.x * teams_per_cta) {
-    if (g.merge && g.info[b] >= 0) continue;
-    const double *C = g.C.item(b);
-    // 1. lower trapezoid of C -> shared (zeros elsewhere in the tri layout)
-    for (int gg = 0; gg < gm; ++gg) {
-      const int w = t.width(gg), base = t.group_off(gg);
-      for (int q = ttid; q < 8 * w; q += tthreads) {
-        const int half = q / (4 * w), rem = q - half * 4 * w;
-        const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
-        double v = 0.0;
-        if (r < m && c < n && c <= r) v = C[eo(g.ci + r, g.cj + c, g.C.cn)];
-        S[base + q] = v;
-      }
+  auto skip = [&](ix b) { return g.merge && g.info[b] >= 0; };
+  ix b = (ix)blockIdx.x * teams_per_cta + team;
+  while (b < g.batch && skip(b)) b += stride;
+  if (b < g.batch) tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+  cp_async_commit();
+  int cur = 0;
+  for (; b < g.batch;) {
+    ix nb = b + stride;
+    while (nb < g.batch && skip(nb)) nb += stride;
+    double *S = cur ? S1 : S0;
+    if (DB && vin) {
+      if (nb < g.batch) tri_load(cur ? S0 : S1, t, g.C.item(nb), g.C.cn, g.ci, g.cj, m, n, gm, true, ttid, tthreads);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     if (ttid == 0) *flag = -1;
     team_sync(bar, tthreads);
@@ -155,13 +189,13 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
           acc[u][0] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc)];
           acc[u][1] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc + 1)];
           const int fa = tri_frag(t, gg, 0, lane), fb = tri_frag(t, jb, 0, lane);
+#pragma unroll 4
           for (int kk = 0; kk < 2 * jb; ++kk) dmma(acc[u], -S[fa + 16 * kk], S[fb + 16 * kk]);
         }
       }
       // diagonal tile (owned by tw == 0, u == 0)
       if (tw == 0) {
         const int f = factor_diag_tile(acc[0], ncol, dinv + 8 * jb, lane);
-        // store the finished columns of the diagonal tile
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * fc + e;
@@ -188,19 +222,39 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
       team_sync(bar, tthreads);
     }
 
-    // 3. write back: the lower trapezoid (or, on failure, exactly what the
+    // write back the lower trapezoid (or, on failure, exactly what the
     // reference's block-row order would have stored, ccore.pyx:884-899)
     double *D = g.D.item(b);
     const int iif = fail >= 0 ? (fail & ~3) : 0;
     if (fail < 0 || aligned_out) {
       for (int gg = 0; gg < gm; ++gg) {
         const int w = t.width(gg), base = t.group_off(gg);
-        for (int q = ttid; q < 8 * w; q += tthreads) {
-          const int half = q / (4 * w), rem = q - half * 4 * w;
-          const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
-          bool st = r < m && c < n && c <= r;
-          if (fail >= 0) st = st && (r < iif || (r < iif + 4 && c < iif));
-          if (st) D[eo(g.di + r, g.dj + c, g.D.cn)] = S[base + q];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int rp = 8 * gg + 4 * half;
+          if (rp >= m) continue;
+          if (vec_out) {
+            for (int q = ttid; q < 2 * w; q += tthreads) {
+              const int c = q >> 1, r0 = rp + 2 * (q & 1);
+              bool w0 = r0 < m && c < n && c <= r0, w1 = r0 + 1 < m && c < n && c <= r0 + 1;
+              if (fail >= 0) {
+                w0 = w0 && (r0 < iif || (r0 < iif + 4 && c < iif));
+                w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && c < iif));
+              }
+              const double *src = S + base + half * 4 * w + 4 * c + 2 * (q & 1);
+              double *dst = D + eo(g.di + r0, g.dj + c, g.D.cn);
+              if (w0 && w1) *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(src);
+              else if (w0) dst[0] = src[0];
+              else if (w1) dst[1] = src[1];
+            }
+          } else {
+            for (int q = ttid; q < 4 * w; q += tthreads) {
+              const int c = q >> 2, r = rp + (q & 3);
+              bool st = r < m && c < n && c <= r;
+              if (fail >= 0) st = st && (r < iif || (r < iif + 4 && c < iif));
+              if (st) D[eo(g.di + r, g.dj + c, g.D.cn)] = S[base + half * 4 * w + q];
+            }
+          }
         }
       }
     }
@@ -209,7 +263,14 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     for (int c = ttid; c < nd; c += tthreads) dA[g.dj + c] = dinv[c];
     if (ttid == 0 && g.info) g.info[b] = fail >= 0 ? fail + g.info_offset : -1;
     team_sync(bar, tthreads);
+    b = nb;
+    if (DB && vin) cur ^= 1;
+    else if (b < g.batch) {
+      tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+      cp_async_commit();
+    }
   }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -309,11 +370,11 @@ static int pick_teams(int tw, ix team_elems, int &threads, size_t &smem) {
   return teams;
 }
 
-template <int TW, int MAXT>
+template <int TW, int MAXT, bool DB>
 static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
-  auto kern = potrf_team_kernel<TW, MAXT>;
+  auto kern = potrf_team_kernel<TW, MAXT, DB>;
   const ix cn8 = (g.n + 7) / 8 * 8;
-  ix team_elems = Tri::size(g.m, g.n) + cn8 + 8;
+  ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8;
   team_elems = (team_elems + 15) / 16 * 16;
   int threads;
   size_t smem;
@@ -326,7 +387,9 @@ static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems);
+  const int vin = (g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0;
+  const int vout = (g.di & 3) == 0 && ((uintptr_t)g.D.p & 15) == 0 && (g.D.stride & 1) == 0;
+  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems, vin, vout);
   note_launch();
   return cudaGetLastError();
 }
@@ -341,12 +404,13 @@ bool potrf_fits(ix m, ix n) {
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   if (potrf_small_ok(g)) return run_potrf_small(g, st);
   const ix gm = (g.m + 7) / 8;
-  if (gm <= 2) return launch_potrf<1, 2>(g, st);
-  if (gm <= 4) return launch_potrf<1, 4>(g, st);
-  if (gm <= 8) return launch_potrf<4, 2>(g, st);
-  if (gm <= 16) return launch_potrf<8, 2>(g, st);
-  if (gm <= 32) return launch_potrf<8, 4>(g, st);
-  return launch_potrf<8, 8>(g, st);
+  const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
+  if (gm <= 2) return db ? launch_potrf<1, 2, true>(g, st) : launch_potrf<1, 2, false>(g, st);
+  if (gm <= 4) return db ? launch_potrf<1, 4, true>(g, st) : launch_potrf<1, 4, false>(g, st);
+  if (gm <= 8) return db ? launch_potrf<4, 2, true>(g, st) : launch_potrf<4, 2, false>(g, st);
+  if (gm <= 16) return launch_potrf<8, 2, false>(g, st);
+  if (gm <= 32) return launch_potrf<8, 4, false>(g, st);
+  return launch_potrf<8, 8, false>(g, st);
 }
 
 bool trsm_fits(ix m, ix n) {

@@ -20,15 +20,19 @@
 // in-tile updates, IEEE sqrt and division, no FMA contraction -- so the
 // factor and diag_inv are bit-identical to the reference's.  Failure
 // index and the partially written factor of a failing item match too.
+#include <cstdlib>
+#include <string>
+
 #include "pb_gemm.cuh"
 
 namespace pb {
 
-template <int N>
+template <int N, int NTH_ = 128, int STAGES_ = 2>
 struct SmallCfg {
   static constexpr int NP = (N + 3) / 4;  // panels
   static constexpr int T = N <= 8 ? 1 : 4;  // threads per item
-  static constexpr int NTHREADS = 128;
+  static constexpr int NTHREADS = NTH_;
+  static constexpr int STAGES = STAGES_;
   static constexpr int ITEMS = NTHREADS / T;
   __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
   __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
@@ -36,7 +40,7 @@ struct SmallCfg {
   static constexpr int STRIDE = ITEM_ELEMS + 2;      // padded (keeps 16-byte alignment)
   static constexpr int BUF = ITEMS * STRIDE;
   static constexpr int DINV = ITEMS * N;  // one round's reciprocals
-  static constexpr size_t SMEM = sizeof(double) * (2 * BUF + DINV) + sizeof(int) * ITEMS;
+  static constexpr size_t SMEM = sizeof(double) * (STAGES * BUF + DINV) + sizeof(int) * ITEMS;
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -227,12 +231,13 @@ __device__ __forceinline__ int factor_t4(double (&L)[4][N], double *dinv, int q,
   return fail;
 }
 
-template <int N>
-__global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(PotrfArgs g) {
-  using Cfg = SmallCfg<N>;
+template <int N, int NTH_, int STAGES_>
+__global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
+  using Cfg = SmallCfg<N, NTH_, STAGES_>;
+  constexpr int STG = Cfg::STAGES;
   constexpr int NP = Cfg::NP, T = Cfg::T, ITEMS = Cfg::ITEMS, STRIDE = Cfg::STRIDE, NTH = Cfg::NTHREADS;
   extern __shared__ __align__(128) double smem[];
-  double *sdinv = smem + 2 * Cfg::BUF;
+  double *sdinv = smem + STG * Cfg::BUF;
   int *sinfo = (int *)(sdinv + Cfg::DINV);
   const int tid = threadIdx.x;
   const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
@@ -246,25 +251,40 @@ __global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(Potr
     const ix b0 = rd * ITEMS;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
+      constexpr int dummy = 0;
+      (void)dummy;
       const int pieces = 2 * Cfg::cols(p);
-      for (int q = tid; q < ITEMS * pieces; q += NTH) {
-        const int it = q / pieces, w = q - it * pieces;
-        const int col = w >> 1, h = w & 1;
-        const ix b = b0 + it;
-        const bool ok = b < g.batch;
-        const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
-        cp_async16(S + it * STRIDE + Cfg::poff(p) + 4 * col + 2 * h, src, ok ? 16 : 0);
+      const int trips = (ITEMS * pieces + NTH - 1) / NTH;
+#pragma unroll
+      for (int k = 0; k < trips; ++k) {
+        const int q = tid + k * NTH;
+        if (q < ITEMS * pieces) {
+          const int it = q / pieces, w = q - it * pieces;
+          const int col = w >> 1, h = w & 1;
+          const ix b = b0 + it;
+          const bool ok = b < g.batch;
+          const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
+          cp_async16(S + it * STRIDE + Cfg::poff(p) + 4 * col + 2 * h, src, ok ? 16 : 0);
+        }
       }
     }
   };
 
-  if (blockIdx.x < nrounds) issue(blockIdx.x, 0);
-  cp_async_commit();
-  int buf = 0;
-  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf ^= 1) {
-    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+#pragma unroll
+  for (int s0 = 0; s0 < STG - 1; ++s0) {
+    const ix r0 = blockIdx.x + (ix)s0 * gridDim.x;
+    if (r0 < nrounds) issue(r0, s0);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  int buf = 0;
+  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf = (buf + 1 == STG ? 0 : buf + 1)) {
+    {
+      const ix rn = rd + (ix)(STG - 1) * gridDim.x;
+      const int bn = (buf + STG - 1) % STG;
+      if (rn < nrounds) issue(rn, bn);
+    }
+    cp_async_commit();
+    cp_async_wait<STG - 1>();
     __syncthreads();
     double *S = smem + buf * Cfg::BUF;
     const int it = tid / T, q = tid % T;
@@ -274,15 +294,26 @@ __global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(Potr
     if constexpr (T == 1) {
       double L[4 * NP][N];
 #pragma unroll
-      for (int r = 0; r < 4 * NP; ++r)
+      for (int p = 0; p < NP; ++p)
 #pragma unroll
-        for (int c = 0; c < N; ++c) L[r][c] = c < Cfg::cols(r >> 2) ? Si[Cfg::poff(r >> 2) + 4 * c + (r & 3)] : 0.0;
+        for (int c = 0; c < N; ++c) {
+          if (c < Cfg::cols(p)) {
+            const double2 lo = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c);
+            const double2 hi = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c + 2);
+            L[4 * p][c] = lo.x, L[4 * p + 1][c] = lo.y, L[4 * p + 2][c] = hi.x, L[4 * p + 3][c] = hi.y;
+          } else {
+            L[4 * p][c] = L[4 * p + 1][c] = L[4 * p + 2][c] = L[4 * p + 3][c] = 0.0;
+          }
+        }
       fail = factor_t1<N>(L, di);
 #pragma unroll
-      for (int r = 0; r < 4 * NP; ++r)
+      for (int p = 0; p < NP; ++p)
 #pragma unroll
         for (int c = 0; c < N; ++c)
-          if (c < Cfg::cols(r >> 2)) Si[Cfg::poff(r >> 2) + 4 * c + (r & 3)] = L[r][c];
+          if (c < Cfg::cols(p)) {
+            *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c) = make_double2(L[4 * p][c], L[4 * p + 1][c]);
+            *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c + 2) = make_double2(L[4 * p + 2][c], L[4 * p + 3][c]);
+          }
     } else {
       double L[4][N];
 #pragma unroll
@@ -293,20 +324,23 @@ __global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(Potr
       for (int p = 0; p < NP; ++p)
         if (p == q) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < N; ++c)
-              if (c < Cfg::cols(p)) L[r][c] = Si[Cfg::poff(p) + 4 * c + r];
+          for (int c = 0; c < N; ++c)
+            if (c < Cfg::cols(p)) {
+              const double2 lo = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c);
+              const double2 hi = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c + 2);
+              L[0][c] = lo.x, L[1][c] = lo.y, L[2][c] = hi.x, L[3][c] = hi.y;
+            }
         }
       fail = factor_t4<N>(L, di, q, (tid & 31) & ~(T - 1));
 #pragma unroll
       for (int p = 0; p < NP; ++p)
         if (p == q) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < N; ++c)
-              if (c < Cfg::cols(p)) Si[Cfg::poff(p) + 4 * c + r] = L[r][c];
+          for (int c = 0; c < N; ++c)
+            if (c < Cfg::cols(p)) {
+              *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c) = make_double2(L[0][c], L[1][c]);
+              *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c + 2) = make_double2(L[2][c], L[3][c]);
+            }
         }
     }
     const ix b0 = rd * ITEMS;
@@ -319,46 +353,68 @@ __global__ void __launch_bounds__(SmallCfg<N>::NTHREADS) potrf_small_kernel(Potr
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const int pieces = 2 * Cfg::cols(p);
-      for (int qq = tid; qq < ITEMS * pieces; qq += NTH) {
-        const int it2 = qq / pieces, w = qq - it2 * pieces;
-        const int col = w >> 1, h = w & 1;
-        const ix bb = b0 + it2;
-        if (bb >= g.batch) continue;
-        const int f = sinfo[it2];
-        const int r0 = 4 * p + 2 * h;
-        bool w0 = r0 >= col && r0 < N, w1 = r0 + 1 >= col && r0 + 1 < N;
-        if (f >= 0) {
-          const int iif = f & ~3;
-          w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
-          w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+      const int trips = (ITEMS * pieces + NTH - 1) / NTH;
+      constexpr int MAXTRIPS = (ITEMS * 2 * N + NTH - 1) / NTH;
+      double2 v[MAXTRIPS];
+#pragma unroll
+      for (int k = 0; k < MAXTRIPS; ++k) {
+        const int qq = tid + k * NTH;
+        if (k < trips && qq < ITEMS * pieces) {
+          const int it2 = qq / pieces, w = qq - it2 * pieces;
+          v[k] = *reinterpret_cast<const double2 *>(S + it2 * STRIDE + Cfg::poff(p) + 4 * (w >> 1) + 2 * (w & 1));
         }
-        const double *src = S + it2 * STRIDE + Cfg::poff(p) + 4 * col + 2 * h;
-        double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
-        if (w0 && w1) {
-          *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(src);
-        } else if (w0) {
-          dst[0] = src[0];
-        } else if (w1) {
-          dst[1] = src[1];
+      }
+#pragma unroll
+      for (int k = 0; k < MAXTRIPS; ++k) {
+        const int qq = tid + k * NTH;
+        if (k < trips && qq < ITEMS * pieces) {
+          const int it2 = qq / pieces, w = qq - it2 * pieces;
+          const int col = w >> 1, h = w & 1;
+          const ix bb = b0 + it2;
+          if (bb < g.batch) {
+            const int f = sinfo[it2];
+            const int r0 = 4 * p + 2 * h;
+            bool w0 = r0 >= col && r0 < N, w1 = r0 + 1 >= col && r0 + 1 < N;
+            if (f >= 0) {
+              const int iif = f & ~3;
+              w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
+              w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+            }
+            double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+            if (w0 && w1) {
+              *reinterpret_cast<double2 *>(dst) = v[k];
+            } else if (w0) {
+              dst[0] = v[k].x;
+            } else if (w1) {
+              dst[1] = v[k].y;
+            }
+          }
         }
       }
     }
     // reciprocals: dA[dj + c] for c < (fail >= 0 ? fail : n)
-    for (int qq = tid; qq < ITEMS * N; qq += NTH) {
-      const int it2 = qq / N, c = qq - it2 * N;
-      const ix bb = b0 + it2;
-      const int f = sinfo[it2];
-      if (bb < g.batch && (f < 0 || c < f)) g.D.d[bb * g.D.dstride + g.dj + c] = sdinv[qq];
+    {
+      constexpr int trips = (ITEMS * N + NTH - 1) / NTH;
+#pragma unroll
+      for (int k = 0; k < trips; ++k) {
+        const int qq = tid + k * NTH;
+        if (qq < ITEMS * N) {
+          const int it2 = qq / N, c = qq - it2 * N;
+          const ix bb = b0 + it2;
+          const int f = sinfo[it2];
+          if (bb < g.batch && (f < 0 || c < f)) g.D.d[bb * g.D.dstride + g.dj + c] = sdinv[qq];
+        }
+      }
     }
     __syncthreads();
   }
   cp_async_wait<0>();
 }
 
-template <int N>
+template <int N, int NTH_ = 128, int STAGES_ = 2>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
-  using Cfg = SmallCfg<N>;
-  auto kern = potrf_small_kernel<N>;
+  using Cfg = SmallCfg<N, NTH_, STAGES_>;
+  auto kern = potrf_small_kernel<N, NTH_, STAGES_>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -374,6 +430,21 @@ static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// tuning hook for the benchmark sweeps (PB_SMALL_CFG = <threads>x<stages>)
+template <int N>
+static cudaError_t launch_small_tuned(const PotrfArgs &g, cudaStream_t st) {
+  const char *e = getenv("PB_SMALL_CFG");
+  if (e) {
+    const std::string v(e);
+    if (v == "64x2") return launch_small<N, 64, 2>(g, st);
+    if (v == "64x3") return launch_small<N, 64, 3>(g, st);
+    if (v == "128x3") return launch_small<N, 128, 3>(g, st);
+    if (v == "256x2") return launch_small<N, 256, 2>(g, st);
+    if (v == "64x4") return launch_small<N, 64, 4>(g, st);
+  }
+  return launch_small<N>(g, st);
+}
+
 bool potrf_small_ok(const PotrfArgs &g) {
   if (g.m != g.n || g.n > 16 || g.n < 1 || g.merge) return false;
   if ((g.ci & 3) || (g.di & 3)) return false;
@@ -387,9 +458,15 @@ cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
 #define PB_SMALL(N_) \
   case N_:           \
     return launch_small<N_>(g, st);
-    PB_SMALL(1) PB_SMALL(2) PB_SMALL(3) PB_SMALL(4) PB_SMALL(5) PB_SMALL(6) PB_SMALL(7) PB_SMALL(8)
-    PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15) PB_SMALL(16)
+    PB_SMALL(1) PB_SMALL(2) PB_SMALL(3) PB_SMALL(5) PB_SMALL(6) PB_SMALL(7)
+    PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15)
 #undef PB_SMALL
+    case 4:
+      return launch_small_tuned<4>(g, st);
+    case 8:
+      return launch_small_tuned<8>(g, st);
+    case 16:
+      return launch_small_tuned<16>(g, st);
     default:
       return cudaErrorInvalidValue;
   }
