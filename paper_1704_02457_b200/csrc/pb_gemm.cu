@@ -287,6 +287,186 @@ __global__ void __launch_bounds__(TiledCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS
 }
 
 // ---------------------------------------------------------------------------
+// gemm_tma: persistent CTAs, TMA bulk-copy pipeline.  In panel-major every
+// (4-row panel x KC-column chunk) of an operand tile is ONE contiguous run
+// of 32*KC bytes, so a stage is a handful of cp.async.bulk copies issued by
+// one warp and tracked by an mbarrier -- no per-element address math.
+// Window rows that do not start on a panel boundary (ai % 4 != 0) copy one
+// extra panel and index fragments with the constant row shift ai % 4, so
+// unaligned stream operands need no repack (level3.py:56-62).
+
+template <int BM, int BN, int WM, int WN, int KC, int STAGES>
+struct TmaCfg {
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NWARPS = WARPS_M * WARPS_N;      // consumer (MMA) warps
+  static constexpr int NTHREADS = 32 * (NWARPS + 1);    // + one producer (TMA) warp
+  static constexpr int MT = WM / 8, NT = WN / 8;
+  static constexpr int PA = BM / 4 + 1, PB = BN / 4 + 1;  // panels per operand tile
+  static constexpr int A_ELEMS = PA * 4 * KC, B_ELEMS = PB * 4 * KC;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES + 16 * STAGES;
+};
+
+// Warp-specialised: warp NWARPS is the producer (bulk copies gated by
+// per-stage "empty" mbarriers), warps 0..NWARPS-1 consume stages gated by
+// "full" mbarriers -- no CTA-wide barrier in the main loop.
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 2)
+    gemm_tma_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES>;
+  constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cfg::STAGE_ELEMS * STAGES);
+  uint64_t *empty = full + STAGES;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const ix ncols = SYRK ? g.m : g.n;
+
+  const ix nk = g.alpha != 0.0 ? (g.k + KC - 1) / KC : 0;
+  const ix steps_per_unit = nk > 0 ? nk : 1;
+  const ix my_units = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const ix nsteps = my_units * steps_per_unit;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::NWARPS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == Cfg::NWARPS) {
+    // ===== producer =====
+    if (nk == 0) return;
+    for (ix s = 0; s < nsteps; ++s) {
+      const int st = (int)(s % STAGES);
+      if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
+      const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
+      const ix ch = s % steps_per_unit;
+      ix b, tm, tn;
+      unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+      double *sa = smem + st * Cfg::STAGE_ELEMS;
+      double *sb = sa + Cfg::A_ELEMS;
+      const ix l0 = ch * KC;
+      const int kc = (int)min((ix)KC, g.k - l0);
+      const ix ra = g.ai + tm * BM, rb = g.bi + tn * BN;
+      const ix rowsa = min((ix)BM, g.m - tm * BM), rowsb = min((ix)BN, ncols - tn * BN);
+      const int npa = (int)(((ra + rowsa - 1) >> 2) - (ra >> 2) + 1);
+      const int npb = (int)(((rb + rowsb - 1) >> 2) - (rb >> 2) + 1);
+      const unsigned bytes = 32u * kc;
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], bytes * (npa + npb));
+      __syncwarp();
+      const double *A = g.A.item(b) + (ra >> 2) * 4 * g.A.cn + 4 * (g.aj + l0);
+      const double *B = g.B.item(b) + (rb >> 2) * 4 * g.B.cn + 4 * (g.bj + l0);
+      for (int p = lane; p < npa + npb; p += 32) {
+        if (p < npa) tma_load_1d(sa + p * 4 * KC, A + (ix)p * 4 * g.A.cn, bytes, &full[st]);
+        else tma_load_1d(sb + (p - npa) * 4 * KC, B + (ix)(p - npa) * 4 * g.B.cn, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int aira = (int)(g.ai & 3), airb = (int)(g.bi & 3);
+  int offa[MT], offb[NT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int r = aira + wm * WM + 8 * i + fr;
+    offa[i] = (r >> 2) * 4 * KC + (r & 3) + 4 * fc;
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int r = airb + wn * WN + 8 * j + fr;
+    offb[j] = (r >> 2) * 4 * KC + (r & 3) + 4 * fc;
+  }
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  ix b = 0, tm = 0, tn = 0;
+  for (ix s = 0; s < nsteps; ++s) {
+    const ix ch = s % steps_per_unit;
+    if (ch == 0) {
+      const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
+      unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+    }
+    const ix rbase = tm * BM + wm * WM, cbase = tn * BN + wn * WN;
+    if (nk > 0) {
+      const int st = (int)(s % STAGES);
+      mbar_wait(&full[st], (unsigned)((s / STAGES) & 1));
+      const double *sa = smem + st * Cfg::STAGE_ELEMS;
+      const double *sb = sa + Cfg::A_ELEMS;
+      const bool active = !SYRK || (cbase <= rbase + WM - 1);
+      const int kc = (int)min((ix)KC, g.k - ch * KC);
+      if (active) {
+        if (kc == KC) {
+#pragma unroll
+          for (int kk = 0; kk < KC / 4; ++kk) {
+            double a[MT], bb[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = sa[offa[i] + 16 * kk];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bb[j] = sb[offb[j] + 16 * kk];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], bb[j]);
+          }
+        } else {
+          for (int kk = 0; 4 * kk < kc; ++kk) {
+            const bool okc = 4 * kk + fc < kc;
+            double a[MT], bb[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = okc ? sa[offa[i] + 16 * kk] : 0.0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bb[j] = okc ? sb[offb[j] + 16 * kk] : 0.0;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], bb[j]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    if (ch == steps_per_unit - 1) {
+      double *D = g.D.item(b);
+      const double *C = g.C.item(b);
+      const bool skip = g.skip && g.skip[b] >= 0;
+      double cv[MT][NT][2];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+            cv[i][j][e] = (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n)) ? ldg_nc(C + eo(g.ci + r, g.cj + c, g.C.cn))
+                                                                          : 0.0;
+          }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+            if (!skip && in_store<SYRK>(r, c, g.m, g.n))
+              D[eo(g.di + r, g.dj + c, g.D.cn)] = epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
+            acc[i][j][e] = 0.0;
+          }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host dispatch
 
 static int g_num_sms = 0;
@@ -348,12 +528,40 @@ static cudaError_t launch_tiled(const GemmArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
+static cudaError_t launch_tma(const GemmArgs &g, cudaStream_t st) {
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES>;
+  auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK>;
+  static bool configured = false;
+  static int occ = 1;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
+    if (occ < 1) occ = 1;
+    configured = true;
+  }
+  const ix tiles_m = (g.m + BM - 1) / BM;
+  const ix tiles_n = SYRK ? tiles_m : (g.n + BN - 1) / BN;
+  const ix per = SYRK ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  const ix nunits = per * g.batch;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > nunits) grid = nunits;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, Cfg::NTHREADS, Cfg::SMEM, st>>>(g, tiles_m, tiles_n, nunits);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <bool SYRK>
 static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   const ix ncols = SYRK ? g.m : g.n;
   const ix big = g.m > ncols ? g.m : ncols;
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
   const ix small = g.m < ncols ? g.m : ncols;
+  if (g.tma) {
+    if (small <= 40) return launch_tma<32, 32, 16, 16, 32, 4, SYRK>(g, st);
+    return launch_tma<64, 64, 32, 16, 32, 3, SYRK>(g, st);
+  }
   if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);
   return launch_tiled<64, 64, 32, 32, 32, 2, SYRK>(g, st);
 }

@@ -11,6 +11,7 @@ struct GemmArgs {
   ix ai, aj, bi, bj, ci, cj, di, dj;
   ix batch;
   bool vecA, vecB;      // 16-byte cp.async legal for the A / B stream
+  bool tma;             // bulk copies legal (16-byte aligned items and panels)
   const int32_t *skip;  // optional: item b is left untouched if skip[b] >= 0
 };
 
