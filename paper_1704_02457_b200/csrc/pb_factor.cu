@@ -103,6 +103,38 @@ __device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double
   return fail;
 }
 
+
+// W = L_jj^{-1} of the 8x8 diagonal block (rows/cols 8j..), written to Wp in
+// panel layout (element (n, k) at (n>>2)*32 + 4k + (n&3)) so that it is read
+// back as the B operand of an m8n8k4 MMA:  X * L_jj^{-T} = X * W^T.  Built by
+// solving the identity against L_jj in registers (one warp, 8 serial steps);
+// columns past ncol stay identity.
+__device__ __forceinline__ void build_inv_block(const double *S, const Tri &t, int j, const double *dinv, int ncol,
+                                                double *Wp, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  double x[2];
+  x[0] = (fr == 2 * fc) ? 1.0 : 0.0;
+  x[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
+  solve_tile_rt(x, S, t, j, dinv, ncol, lane);  // x = I * L^{-T}: x[r][c] = Linv[c][r]
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * fc + e, k = fr;
+    Wp[(n >> 2) * 32 + 4 * k + (n & 3)] = x[e];
+  }
+}
+
+// acc := X * W^T for an 8x8 tile X held in shared memory (tri layout, rows
+// 8g.., cols 8j..) and W from build_inv_block.
+__device__ __forceinline__ void apply_inv_block(double (&acc)[2], const double *S, const Tri &t, int g, int j,
+                                                const double *Wp, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  const int fa = tri_frag(t, g, 0, lane) + 32 * j;  // column block j starts at 4*8j
+  const int fb = (lane >> 4) * 32 + 4 * fc + (fr & 3);
+  acc[0] = acc[1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) dmma(acc, S[fa + 16 * kk], Wp[fb + 16 * kk]);
+}
+
 // ---------------------------------------------------------------------------
 // potrf team kernel
 
@@ -152,6 +184,7 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   double *S1 = DB ? S0 + tri_elems : S0;
   double *dinv = S0 + (DB ? 2 : 1) * tri_elems;         // cn8 doubles
   volatile int *flag = (volatile int *)(dinv + t.cn8);  // failure index
+  double *Wp = dinv + t.cn8 + 8;                        // inverted diagonal block (64)
   const int fr = lane >> 2, fc = lane & 3;
   const bool aligned_out = (g.di & 3) == 0;
   const bool vin = vec_in != 0;
@@ -193,7 +226,8 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
           for (int kk = 0; kk < 2 * jb; ++kk) dmma(acc[u], -S[fa + 16 * kk], S[fb + 16 * kk]);
         }
       }
-      // diagonal tile (owned by tw == 0, u == 0)
+      // diagonal tile (owned by tw == 0, u == 0): factor, then its inverse;
+      // the other tiles park their downdated values in shared memory
       if (tw == 0) {
         const int f = factor_diag_tile(acc[0], ncol, dinv + 8 * jb, lane);
 #pragma unroll
@@ -202,16 +236,27 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
           if (c < ncol && (f < 0 || c < f)) S[t.off(8 * jb + fr, 8 * jb + c)] = acc[0][e];
         }
         if (f >= 0 && lane == 0) *flag = 8 * jb + f;
+        __syncwarp();
+        if (f < 0 && jb + 1 < gm) build_inv_block(S, t, jb, dinv, ncol, Wp, lane);
       }
-      team_sync(bar, tthreads);
-      fail = *flag;
-      if (fail >= 0) break;
-      // solve the tiles below the diagonal
 #pragma unroll
       for (int u = 0; u < MAXT; ++u) {
         const int gg = jb + tw + u * TW;
         if (gg < gm && gg > jb) {
-          solve_tile_rt(acc[u], S, t, jb, dinv, ncol, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) S[t.off(8 * gg + fr, 8 * jb + 2 * fc + e)] = acc[u][e];
+        }
+      }
+      team_sync(bar, tthreads);
+      fail = *flag;
+      if (fail >= 0) break;
+      // solve the tiles below the diagonal: X := X * L_jj^{-T} on DMMA
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int gg = jb + tw + u * TW;
+        if (gg < gm && gg > jb) {
+          apply_inv_block(acc[u], S, t, gg, jb, Wp, lane);
+          __syncwarp();
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 2 * fc + e;
@@ -277,7 +322,7 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
 // trsm_rltn team kernel: D * A^T = alpha * B
 
 template <int TW>
-__global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_elems) {
+__global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_elems, int vec_in) {
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int team = warp / TW, tw = warp % TW;
@@ -291,25 +336,17 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
   const int tri_elems = (int)Tri::size(n, n);
   double *S = smem + (ix)team * team_elems;
   double *dinv = S + tri_elems;
-  volatile int *flag = (volatile int *)(dinv + t.cn8);
-  double *strip = dinv + t.cn8 + 8 + tw * 8 * t.cn8;  // this warp's solved rows, 2 panels x cn8
+  double *Wall = dinv + t.cn8 + 8;                      // gn inverted diagonal blocks
+  double *strip = Wall + 64 * t.gn + tw * 8 * t.cn8;    // this warp's rows, 2 panels x cn8
   const int fr = lane >> 2, fc = lane & 3;
   const int gmr = (m + 7) / 8;
+  const int fa = (lane >> 4) * 4 * t.cn8 + 4 * fc + ((lane >> 2) & 3);
 
   for (ix b = (ix)blockIdx.x * teams_per_cta + team; b < g.batch; b += (ix)gridDim.x * teams_per_cta) {
     if (g.skip && g.skip[b] >= 0) continue;
-    const double *A = g.A.item(b);
-    for (int gg = 0; gg < t.gn; ++gg) {
-      const int w = t.width(gg), base = t.group_off(gg);
-      for (int q = ttid; q < 8 * w; q += tthreads) {
-        const int half = q / (4 * w), rem = q - half * 4 * w;
-        const int c = rem >> 2, r = 8 * gg + 4 * half + (rem & 3);
-        double v = 0.0;
-        if (r < n && c <= r) v = A[eo(g.ai + r, g.aj + c, g.A.cn)];
-        S[base + q] = v;
-      }
-    }
-    if (ttid == 0) *flag = -1;
+    tri_load(S, t, g.A.item(b), g.A.cn, g.ai, g.aj, n, n, t.gn, vec_in != 0, ttid, tthreads);
+    cp_async_commit();
+    cp_async_wait<0>();
     team_sync(bar, tthreads);
     // reciprocals: reuse the factorization's, or compute (zero -> info)
     if (g.use_dA) {
@@ -326,22 +363,33 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
         if (S[t.off(c, c)] == 0.0) { fail = c; break; }
     }
     if (fail < 0) {
+      // inverse of every 8x8 diagonal block, spread over the team's warps
+      for (int jb = tw; jb < t.gn; jb += TW) build_inv_block(S, t, jb, dinv, min(8, n - 8 * jb), Wall + 64 * jb, lane);
+      team_sync(bar, tthreads);
       const double *B = g.B.item(b);
       double *D = g.D.item(b);
       for (int gg = tw; gg < gmr; gg += TW) {
+        const int r = 8 * gg + fr;
         for (int jb = 0; jb < t.gn; ++jb) {
-          const int ncol = min(8, n - 8 * jb);
           double x[2];
-          const int r = 8 * gg + fr;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 8 * jb + 2 * fc + e;
             x[e] = (r < m && c < n) ? __dmul_rn(g.alpha, B[eo(g.bi + r, g.bj + c, g.B.cn)]) : 0.0;
           }
-          const int fa = (lane >> 4) * 4 * t.cn8 + 4 * fc + ((lane >> 2) & 3);
           const int fb = tri_frag(t, jb, 0, lane);
+#pragma unroll 4
           for (int kk = 0; kk < 2 * jb; ++kk) dmma(x, -strip[fa + 16 * kk], S[fb + 16 * kk]);
-          solve_tile_rt(x, S, t, jb, dinv, ncol, lane);
+          // x := x * L_jj^{-T} via the inverted block (two DMMAs)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) strip[((fr >> 2) * 4 * t.cn8) + 4 * (8 * jb + 2 * fc + e) + (fr & 3)] = x[e];
+          __syncwarp();
+          const double *W = Wall + 64 * jb;
+          const int fw = (lane >> 4) * 32 + 4 * fc + (fr & 3);
+          x[0] = x[1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) dmma(x, strip[fa + 32 * jb + 16 * kk], W[fw + 16 * kk]);
+          __syncwarp();
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 8 * jb + 2 * fc + e;
@@ -374,7 +422,7 @@ template <int TW, int MAXT, bool DB>
 static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
   auto kern = potrf_team_kernel<TW, MAXT, DB>;
   const ix cn8 = (g.n + 7) / 8 * 8;
-  ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8;
+  ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8 + 64;
   team_elems = (team_elems + 15) / 16 * 16;
   int threads;
   size_t smem;
@@ -396,7 +444,7 @@ static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
 
 bool potrf_fits(ix m, ix n) {
   const ix cn8 = (n + 7) / 8 * 8;
-  const ix e = Tri::size(m, n) + cn8 + 8;
+  const ix e = Tri::size(m, n) + cn8 + 8 + 64;
   const ix gm = (m + 7) / 8;
   return e * 8 <= 220 * 1024 && gm <= 8 * 8;
 }
@@ -416,7 +464,7 @@ cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
 bool trsm_fits(ix m, ix n) {
   (void)m;
   const ix cn8 = (n + 7) / 8 * 8;
-  const ix e = Tri::size(n, n) + cn8 + 8 + 8 * 8 * cn8;
+  const ix e = Tri::size(n, n) + cn8 + 8 + 64 * (cn8 / 8) + 8 * 8 * cn8;
   return e * 8 <= 220 * 1024;
 }
 
@@ -424,7 +472,7 @@ template <int TW>
 static cudaError_t launch_trsm(const TrsmArgs &g, cudaStream_t st) {
   auto kern = trsm_team_kernel<TW>;
   const ix cn8 = (g.n + 7) / 8 * 8;
-  ix team_elems = Tri::size(g.n, g.n) + cn8 + 8 + (ix)TW * 8 * cn8;
+  ix team_elems = Tri::size(g.n, g.n) + cn8 + 8 + 64 * (cn8 / 8) + (ix)TW * 8 * cn8;
   team_elems = (team_elems + 15) / 16 * 16;
   int threads;
   size_t smem;
@@ -437,7 +485,8 @@ static cudaError_t launch_trsm(const TrsmArgs &g, cudaStream_t st) {
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems);
+  const int vin = (g.ai & 3) == 0 && ((uintptr_t)g.A.p & 15) == 0 && (g.A.stride & 1) == 0;
+  kern<<<(unsigned)grid, threads, smem, st>>>(g, (int)team_elems, vin);
   note_launch();
   return cudaGetLastError();
 }
