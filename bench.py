@@ -362,8 +362,8 @@ def traffic_from_profile(pt):
     """dram bytes per launch from a committed ncu capture, if one exists."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(pt.label)
+        d = json.load(open(p))[pt.label]
+        return d["dram_bytes_per_launch"] * pt.chunk / d["items_per_launch"]
     except Exception:
         return None
 
