@@ -9,6 +9,7 @@
 // downdate + recursive trailing factor; trsm: column-block solve + gemm
 // downdate), so every size the reference accepts runs on the GPU.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 

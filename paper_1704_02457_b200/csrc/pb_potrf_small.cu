@@ -37,7 +37,7 @@ struct SmallCfg {
   __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
   __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
   static constexpr int ITEM_ELEMS = poff(NP);        // lower-prefix doubles per item
-  static constexpr int STRIDE = ITEM_ELEMS + 2;      // padded (keeps 16-byte alignment)
+  static constexpr int STRIDE = ITEM_ELEMS + 2;      // padded (16-byte aligned, odd 16-byte units)
   static constexpr int BUF = ITEMS * STRIDE;
   static constexpr int DINV = ITEMS * N;  // one round's reciprocals
   static constexpr size_t SMEM = sizeof(double) * (STAGES * BUF + DINV) + sizeof(int) * ITEMS;
@@ -349,44 +349,72 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
       if (b0 + it < g.batch && g.info) g.info[b0 + it] = fail;
     }
     __syncthreads();
-    // masked, coalesced stores of the lower triangle (the reference's write set)
+    // Stores of the reference's write set (lower triangle; on failure only
+    // what the reference stored before returning).  Columns left of a
+    // panel's diagonal block are entirely lower: full 16-byte pieces.  The
+    // diagonal 4x4 block holds strict-upper bytes that must stay untouched:
+    // masked stores there (the L2 fills those chunks from DRAM; a software
+    // read-modify-write of D was measured slower -- see DESIGN.md).
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const int pieces = 2 * Cfg::cols(p);
-      const int trips = (ITEMS * pieces + NTH - 1) / NTH;
-      constexpr int MAXTRIPS = (ITEMS * 2 * N + NTH - 1) / NTH;
-      double2 v[MAXTRIPS];
+      // (1) off-diagonal columns [0, 4p)
+      {
+        const int pieces = 8 * p;
+        const int trips = (ITEMS * pieces + NTH - 1) / NTH;
+        constexpr int MAXTRIPS = (ITEMS * 8 * (NP - 1) + NTH - 1) / NTH;
 #pragma unroll
-      for (int k = 0; k < MAXTRIPS; ++k) {
-        const int qq = tid + k * NTH;
-        if (k < trips && qq < ITEMS * pieces) {
-          const int it2 = qq / pieces, w = qq - it2 * pieces;
-          v[k] = *reinterpret_cast<const double2 *>(S + it2 * STRIDE + Cfg::poff(p) + 4 * (w >> 1) + 2 * (w & 1));
+        for (int k = 0; k < (MAXTRIPS > 0 ? MAXTRIPS : 1); ++k) {
+          const int qq = tid + k * NTH;
+          if (k < trips && qq < ITEMS * pieces) {
+            const int it2 = qq / pieces, w = qq - it2 * pieces;
+            const int col = w >> 1, h = w & 1;
+            const ix bb = b0 + it2;
+            if (bb < g.batch) {
+              const double2 v = *reinterpret_cast<const double2 *>(S + it2 * STRIDE + Cfg::poff(p) + 4 * col + 2 * h);
+              const int f = sinfo[it2];
+              const int r0 = 4 * p + 2 * h;
+              bool w0 = r0 < N, w1 = r0 + 1 < N;
+              if (f >= 0) {
+                const int iif = f & ~3;
+                w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
+                w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+              }
+              double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+              if (w0 && w1) *reinterpret_cast<double2 *>(dst) = v;
+              else if (w0) dst[0] = v.x;
+              else if (w1) dst[1] = v.y;
+            }
+          }
         }
       }
+      // (2) the diagonal block, columns [4p, 4p+4)
+      {
+        constexpr int trips = (ITEMS * 8 + NTH - 1) / NTH;
 #pragma unroll
-      for (int k = 0; k < MAXTRIPS; ++k) {
-        const int qq = tid + k * NTH;
-        if (k < trips && qq < ITEMS * pieces) {
-          const int it2 = qq / pieces, w = qq - it2 * pieces;
-          const int col = w >> 1, h = w & 1;
-          const ix bb = b0 + it2;
-          if (bb < g.batch) {
-            const int f = sinfo[it2];
-            const int r0 = 4 * p + 2 * h;
-            bool w0 = r0 >= col && r0 < N, w1 = r0 + 1 >= col && r0 + 1 < N;
-            if (f >= 0) {
-              const int iif = f & ~3;
-              w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
-              w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
-            }
-            double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
-            if (w0 && w1) {
-              *reinterpret_cast<double2 *>(dst) = v[k];
-            } else if (w0) {
-              dst[0] = v[k].x;
-            } else if (w1) {
-              dst[1] = v[k].y;
+        for (int k = 0; k < trips; ++k) {
+          const int qq = tid + k * NTH;
+          if (qq < ITEMS * 8) {
+            const int it2 = qq >> 3, w = qq & 7;
+            const int cl = w >> 1, h = w & 1, col = 4 * p + cl;
+            const ix bb = b0 + it2;
+            if (bb < g.batch && col < Cfg::cols(p)) {
+              const double *Si2 = S + it2 * STRIDE;
+              const int f = sinfo[it2];
+              const int iif = f >= 0 ? (f & ~3) : 0;
+              double val[2];
+              bool wr[2];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int r = 4 * p + 2 * h + i;
+                bool wi = r >= col && r < N && col < N;
+                if (f >= 0) wi = wi && (r < iif || (r < iif + 4 && col < iif));
+                wr[i] = wi;
+                val[i] = Si2[Cfg::poff(p) + 4 * col + 2 * h + i];
+              }
+              double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+              if (wr[0] && wr[1]) *reinterpret_cast<double2 *>(dst) = make_double2(val[0], val[1]);
+              else if (wr[0]) dst[0] = val[0];
+              else if (wr[1]) dst[1] = val[1];
             }
           }
         }
