@@ -166,7 +166,10 @@ __device__ __forceinline__ void tri_load(double *S, const Tri &t, const double *
   }
 }
 
-template <int TW, int MAXT, bool DB>
+// GM/GN > 0 fix the row/column group counts at compile time (the common
+// square sizes): every tile loop then unrolls and all tri-layout offsets
+// fold to constants; GM = GN = 0 is the generic runtime-shaped kernel.
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0>
 __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -176,10 +179,10 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   const int bar = 1 + team;
   const int m = (int)g.m, n = (int)g.n;
   Tri t;
-  t.cn8 = (n + 7) / 8 * 8;
-  t.gn = t.cn8 / 8;
-  const int gm = (m + 7) / 8;
-  const int tri_elems = (int)Tri::size(m, n);
+  t.cn8 = GN > 0 ? 8 * GN : (n + 7) / 8 * 8;
+  t.gn = GN > 0 ? GN : t.cn8 / 8;
+  const int gm = GM > 0 ? GM : (m + 7) / 8;
+  const int tri_elems = GM > 0 ? (int)Tri::size(8 * GM, 8 * GN) : (int)Tri::size(m, n);
   double *S0 = smem + (ix)team * team_elems;
   double *S1 = DB ? S0 + tri_elems : S0;
   double *dinv = S0 + (DB ? 2 : 1) * tri_elems;         // cn8 doubles
@@ -211,7 +214,9 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     team_sync(bar, tthreads);
 
     int fail = -1;
-    for (int jb = 0; jb < t.gn; ++jb) {
+#pragma unroll(GN > 0 ? GN : 1)
+    for (int jb = 0; jb < (GN > 0 ? GN : 64); ++jb) {
+      if (GN == 0 && jb >= t.gn) break;
       const int ncol = min(8, n - 8 * jb);
       double acc[MAXT][2];
       // downdate every row-group tile of this column block this warp owns
@@ -418,9 +423,9 @@ static int pick_teams(int tw, ix team_elems, int &threads, size_t &smem) {
   return teams;
 }
 
-template <int TW, int MAXT, bool DB>
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0>
 static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
-  auto kern = potrf_team_kernel<TW, MAXT, DB>;
+  auto kern = potrf_team_kernel<TW, MAXT, DB, GM, GN>;
   const ix cn8 = (g.n + 7) / 8 * 8;
   ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8 + 64;
   team_elems = (team_elems + 15) / 16 * 16;
@@ -453,6 +458,10 @@ cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   if (potrf_small_ok(g)) return run_potrf_small(g, st);
   const ix gm = (g.m + 7) / 8;
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
+  const ix gn = (g.n + 7) / 8;
+  // compile-time shaped instances for the common (benchmark) sizes
+  if (gm == 4 && gn == 4) return launch_potrf<1, 4, true, 4, 4>(g, st);
+  if (gm == 8 && gn == 8) return launch_potrf<4, 2, true, 8, 8>(g, st);
   if (gm <= 2) return db ? launch_potrf<1, 2, true>(g, st) : launch_potrf<1, 2, false>(g, st);
   if (gm <= 4) return db ? launch_potrf<1, 4, true>(g, st) : launch_potrf<1, 4, false>(g, st);
   if (gm <= 8) return db ? launch_potrf<4, 2, true>(g, st) : launch_potrf<4, 2, false>(g, st);
