@@ -35,6 +35,7 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+GRAPH_LAUNCHES = [0]  # kernels launched through CUDA-graph replay (not seen by the ABI counter)
 FP64_PEAK_GFLOPS = 37150.0  # measured DMMA/DFMA microbench, profiles/r01_fp64_peak.log
 FP64_PEAK_SRC = "measured (tools/fp64_peak.cu, DMMA m8n8k4 37.15 TF/s; cuBLAS DGEMM 35.5 TF/s)"
 
@@ -83,6 +84,14 @@ class Point:
             self.flops_item = float(m) * n * n
             self.bytes_item = 8.0 * (n * (n + 1) / 2 + n + 2 * m * n)
             self.io_bytes = memsize(n, n) + 2 * memsize(m, n)
+        elif op == "riccati":  # m = nx, n = nu, k = N stages
+            nx, nu, ns = m, n, m + n
+            per_stage = (2.0 * ns * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0 + float(nx) * nu * nu
+                         + 2.0 * nx * nx * nx)
+            self.flops_item = k * per_stage
+            # per stage: read BAt,P,RQ,W,M,F; write W,M,F,K,P (algorithmic, lower halves where symmetric)
+            self.bytes_item = k * 8.0 * (2 * ns * nx + 2 * nx * nx + 3 * ns * (ns + 1) / 2 + ns * nx + nx * nu)
+            self.io_bytes = 8 * memsize(ns, ns)
         else:
             raise ValueError(op)
         self.reps = max(1, math.ceil(batch * self.io_bytes / cap_bytes))
@@ -90,6 +99,8 @@ class Point:
 
     @property
     def label(self):
+        if self.op == "riccati":
+            return f"riccati nx={self.m} nu={self.n} N={self.k}"
         if self.op == "potrf_l":
             return f"potrf_l n={self.n}"
         if self.op == "gemm_nt":
@@ -114,6 +125,9 @@ def config_points(name):
     if name == "c4":
         return [Point("syrk_ln", 96, 96, 40, 8192, -1.0, 1.0), Point("trsm_rltn", 72, 48, 0, 8192, 1.0)], \
             "C4 dsyrk_ln 96x40 at (3,1) alpha=-1 beta=1 + dtrsm_rltn 72x48 (diag_inv reused), batch 8192"
+    if name == "c5":
+        return [Point("riccati", 32, 8, 50, 1024)], \
+            "C5 Riccati-style chain: 1024 problems x N=50 stages, nx=32 nu=8 (gemm_nt, syrk_ln, potrf_l, trsm_rltn, gemm_nt per stage)"
     raise SystemExit(f"unknown config {name}")
 
 
@@ -167,6 +181,28 @@ class GpuPoint:
             self.C = pb.allocate_panel_batch(nb, m, m, device=device)
             self.C.storage.uniform_(-1, 1, generator=g)
             self.D = pb.allocate_panel_batch(nb, m, m, device=device, zero=True)
+        elif pt.op == "riccati":
+            from paper_1704_02457_b200.chain import RiccatiChain
+            nx, nu = m, n
+            Ad = torch.randn((nb, nx, nx), dtype=torch.float64, device=device, generator=g)
+            rho = torch.linalg.eigvals(Ad).abs().amax(dim=1)
+            Ad *= (0.95 / rho)[:, None, None]
+            Bd = torch.randn((nb, nx, nu), dtype=torch.float64, device=device, generator=g)
+            G = torch.randn((nb, nx, nx), dtype=torch.float64, device=device, generator=g)
+            H = torch.randn((nb, nu, nu), dtype=torch.float64, device=device, generator=g)
+            Q = 0.1 * torch.eye(nx, dtype=torch.float64, device=device) + G @ G.transpose(1, 2) / nx
+            R = torch.eye(nu, dtype=torch.float64, device=device) + H @ H.transpose(1, 2) / nu
+            ch = RiccatiChain(nb, nx, nu, device=device)
+            pack.pack_array_into(torch.cat([Bd.transpose(1, 2), Ad.transpose(1, 2)], dim=1).contiguous(), ch.BAt)
+            RQ = torch.zeros((nb, nx + nu, nx + nu), dtype=torch.float64, device=device)
+            RQ[:, :nu, :nu] = R
+            RQ[:, nu:, nu:] = Q
+            pack.pack_array_into(RQ, ch.RQ)
+            self.Q = pb.allocate_panel_batch(nb, nx, nx, device=device)
+            pack.pack_array_into(Q.contiguous(), self.Q)
+            ch.P.storage.copy_(self.Q.storage)
+            ch.capture(k)
+            self.chain = ch
         elif pt.op == "trsm_rltn":
             from paper_1704_02457_b200 import level3
             M = u(nb, n, n)
@@ -201,6 +237,11 @@ class GpuPoint:
                 level3.syrk_ln(pt.m, pt.k, pt.alpha, a, a, pt.beta, self.C, self.D)
             elif pt.op == "trsm_rltn":
                 level3.trsm_rltn(pt.m, pt.n, pt.alpha, self.A, self.B, self.D, check=False)
+            elif pt.op == "riccati":
+                # P_N = Q, then the captured N-stage sweep (one graph launch of 5N kernels)
+                self.chain.P.storage.copy_(self.Q.storage)
+                self.chain.replay()
+                GRAPH_LAUNCHES[0] += 5 * pt.k
 
 
 def nvsmi_sampler(path):
@@ -279,13 +320,14 @@ def run_ours(args):
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     _native.launch_count(reset=True)
+    GRAPH_LAUNCHES[0] = 0
     torch.cuda.synchronize()
     t0.record(stream)
     for s in range(args.steps):
         step([evs[s][i] for i in range(len(gps))])
     t1.record(stream)
     torch.cuda.synchronize()
-    launches = _native.launch_count()
+    launches = _native.launch_count() + GRAPH_LAUNCHES[0]
     if sampler:
         sampler.terminate()
         sampler.wait()
@@ -486,6 +528,30 @@ def _cpu_worker(job):
             call = lambda c: lib.po_potrf_l(L(n), L(n), c.ctypes.data_as(O.ctypes.c_void_p), L(0), L(0), L(ck), Dp,  # noqa: E731,E501
                                             L(0), L(0), L(ck), vp, L(0))
         flops_item = n ** 3 / 3.0
+    elif op == "riccati":
+        nx, nu, N = m, n, k
+        ns = nx + nu
+        sdx, sds, sdu = -(-nx // 4) * 4, -(-ns // 4) * 4, -(-nu // 4) * 4
+        rs = -(-ns // 4) * 4
+        BAt = rng.standard_normal(rs * sdx)
+        RQ = np.zeros(rs * sds)
+        ii = np.arange(ns)
+        RQ[(ii - (ii & 3)) * sds + 4 * ii + (ii & 3)] = 1.0 + ns
+        P = np.zeros(sdx * sdx)
+        P[(np.arange(nx) - (np.arange(nx) & 3)) * sdx + 4 * np.arange(nx) + (np.arange(nx) & 3)] = 1.0
+        W, M, F = np.zeros(rs * sdx), np.zeros(rs * sds), np.zeros(rs * sds)
+        K, dv = np.zeros(sdx * sdu), np.zeros(ns)
+
+        def call(c):
+            for _ in range(N):
+                core.gemm_nt_drv(ns, nx, nx, 1.0, BAt, 0, 0, sdx, P, 0, 0, sdx, 0.0, W, 0, 0, sdx, W, 0, 0, sdx)
+                core.syrk_ln_drv(ns, nx, 1.0, W, 0, 0, sdx, BAt, 0, 0, sdx, 1.0, RQ, 0, 0, sds, M, 0, 0, sds)
+                core.potrf_drv(ns, ns, M, 0, 0, sds, F, 0, 0, sds, dv, 0)
+                core.trsm_rltn_drv(nx, nu, -1.0, F, 0, 0, sds, False, F, nu, 0, sds, K, 0, 0, sdu, dv, 0)
+                core.gemm_nt_drv(nx, nx, nx, 1.0, F, nu, nu, sds, F, nu, nu, sds, 0.0, P, 0, 0, sdx, P, 0, 0, sdx)
+        flops_item = N * (2.0 * ns * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0 + float(nx) * nu * nu
+                          + 2.0 * nx * nx * nx)
+        Cs = [None]
     else:
         sdk = -(-k // 4) * 4 if op != "trsm_rltn" else cn
         A = rng.uniform(-1, 1, ru(m + 4) * max(sdk, cn, 4) + 64)

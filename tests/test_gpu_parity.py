@@ -480,3 +480,39 @@ def test_potrf_small_bit_exact(n):
     winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
     assert np.array_equal(info, winfo)
     assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64))
+
+
+def test_riccati_chain_c5_vs_oracle_and_graph_replay():
+    """C5 chain: gemm_nt -> syrk_ln -> potrf_l -> trsm_rltn ->
+    gemm_nt per stage, batched over problems; eager and CUDA-graph replay are
+    bit-identical, and both match the oracle chain."""
+    from chain_util import make_problems, oracle_chain, packed_inputs
+    from paper_1704_02457_b200.chain import RiccatiChain
+    nb, nx, nu, N = 16, 32, 8, 50
+    A, B, Q, R = make_problems(nb, nx, nu, seed=3)
+    BAt, RQ, P0 = packed_inputs(A, B, Q, R)
+
+    def fresh():
+        ch = RiccatiChain(nb, nx, nu)
+        pack.pack_array_into(torch.from_numpy(BAt).cuda(), ch.BAt)
+        pack.pack_array_into(torch.from_numpy(RQ).cuda(), ch.RQ)
+        pack.pack_array_into(torch.from_numpy(P0).cuda(), ch.P)
+        return ch
+
+    ch = fresh()
+    ch.run(N)
+    P = pack.panel_to_array(ch.P).cpu().numpy()
+    K = pack.panel_to_array(ch.K).cpu().numpy()
+    Pw, Kw = oracle_chain(BAt, RQ, P0, nx, nu, N)
+    fp_close(P, Pw, nx + nu, "C5 P_0")
+    fp_close(K, Kw, nx + nu, "C5 K")
+    g = fresh()
+    g.capture(N)  # capture records N stages after one warm-up stage
+    g2 = fresh()
+    g2.graph = g.graph
+    # replaying the graph re-runs exactly the captured launches on g's buffers
+    g.P.storage.copy_(g2.P.storage)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(g.P.storage, ch.P.storage)
+    assert torch.equal(g.K.storage, ch.K.storage)

@@ -155,3 +155,15 @@ def test_oracle_potrf_against_numpy():
         assert O.rel_fro(got, np.linalg.cholesky(a)) < O.tol(n)
         dinv = D.storage[0, D.diag_off: D.diag_off + n]
         assert np.max(np.abs(dinv * np.diag(got) - 1.0)) <= 1e-15  # tests/test_acceptance.py:266-267
+
+
+def test_oracle_chain_matches_dense_riccati():
+    """The C5 chain run on the oracle equals the dense
+    Riccati recursion: P_next = Q + A'PA - A'PB (R + B'PB)^-1 B'PA."""
+    from chain_util import dense_riccati, make_problems, oracle_chain, packed_inputs
+    A, B, Q, R = make_problems(3, 32, 8, seed=1)
+    BAt, RQ, P0 = packed_inputs(A, B, Q, R)
+    P, K = oracle_chain(BAt, RQ, P0, 32, 8, 12)
+    Pd = dense_riccati(A, B, Q, R, 12)
+    Pfull = np.tril(P) + np.tril(P, -1).transpose(0, 2, 1)
+    assert np.max(np.abs(Pfull - Pd)) / np.max(np.abs(Pd)) < 1e-12
