@@ -116,6 +116,7 @@ static int gemm_common(bool syrk, int m, int n, int k, double alpha, const pb_dm
   g.vecA = vec16_ok(sA, ai);
   g.vecB = vec16_ok(sB, bi);
   g.tma = tma_ok(sA) && tma_ok(sB);
+  g.tmaC = tma_ok(sC);
   g.skip = skip;
   cudaStream_t st = (cudaStream_t)stream;
   return finish(syrk ? run_syrk_ln(g, st) : run_gemm_nt(g, st));
@@ -162,6 +163,7 @@ static int trsm_run(int m, int n, double alpha, const pb_dmat_batch *sA, int ai,
   g.vecA = vec16_ok(sD, di);
   g.vecB = vec16_ok(sA, ai + n1);
   g.tma = tma_ok(sD) && tma_ok(sA);
+  g.tmaC = tma_ok(sB);
   g.skip = skip;
   if ((r = finish(run_gemm_nt(g, st)))) return r;
   return trsm_run(m, n - n1, 1.0, sA, ai + n1, aj + n1, use_dA, sD, di, dj + n1, sD, di, dj + n1, nullptr, skip, st);
@@ -225,6 +227,7 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
   g.batch = sD->batch;
   g.vecA = g.vecB = vec16_ok(sD, di + n1);
   g.tma = tma_ok(sD);
+  g.tmaC = tma_ok(sC);
   g.skip = info;
   if ((r = finish(run_syrk_ln(g, st)))) return r;
   return potrf_run(m - n1, n - n1, sD, di + n1, dj + n1, sD, di + n1, dj + n1, info, 1, off + n1, st);

@@ -22,6 +22,9 @@
 // the m x n window (syrk: lower triangle only), unaligned row origins are
 // gathered in-kernel instead of the reference's host repack
 // (level3.py:56-62).
+#include <cstdlib>
+#include <string>
+
 #include "pb_gemm.cuh"
 
 namespace pb {
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(TiledCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS
 // extra panel and index fragments with the constant row shift ai % 4, so
 // unaligned stream operands need no repack (level3.py:56-62).
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, int CB>
 struct TmaCfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NWARPS = WARPS_M * WARPS_N;      // consumer (MMA) warps
@@ -304,22 +307,30 @@ struct TmaCfg {
   static constexpr int PA = BM / 4 + 1, PB = BN / 4 + 1;  // panels per operand tile
   static constexpr int A_ELEMS = PA * 4 * KC, B_ELEMS = PB * 4 * KC;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES + 16 * STAGES;
+  static constexpr int C_ELEMS = PA * 4 * BN;            // one C tile (panels x BN columns)
+  static constexpr size_t SMEM = sizeof(double) * (STAGE_ELEMS * STAGES + C_ELEMS * CB) + 16 * (STAGES + CB);
 };
 
 // Warp-specialised: warp NWARPS is the producer (bulk copies gated by
 // per-stage "empty" mbarriers), warps 0..NWARPS-1 consume stages gated by
-// "full" mbarriers -- no CTA-wide barrier in the main loop.
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
-__global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 2)
+// "full" mbarriers -- no CTA-wide barrier in the main loop.  With CB > 0
+// the producer also streams each unit's C tile into one of CB shared
+// buffers, so the epilogue reads C from shared memory instead of waiting
+// on global loads.
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREADS, (CB >= 2 ? 1 : 2))
     gemm_tma_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
-  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES>;
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
   extern __shared__ __align__(128) double smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Cfg::STAGE_ELEMS * STAGES);
+  double *cbuf = smem + Cfg::STAGE_ELEMS * STAGES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(cbuf + Cfg::C_ELEMS * CB);
   uint64_t *empty = full + STAGES;
+  uint64_t *cfull = empty + STAGES;
+  uint64_t *cempty = cfull + CB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const ix ncols = SYRK ? g.m : g.n;
+  const bool cin = CB > 0 && g.beta != 0.0 && g.tmaC;  // C through shared memory
 
   const ix nk = g.alpha != 0.0 ? (g.k + KC - 1) / KC : 0;
   const ix steps_per_unit = nk > 0 ? nk : 1;
@@ -332,20 +343,39 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::NWARPS);
     }
+#pragma unroll
+    for (int s = 0; s < CB; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], Cfg::NWARPS);
+    }
     mbar_fence_init();
   }
   __syncthreads();
 
   if (warp == Cfg::NWARPS) {
     // ===== producer =====
-    if (nk == 0) return;
+    if (nk == 0 && !cin) return;
     for (ix s = 0; s < nsteps; ++s) {
-      const int st = (int)(s % STAGES);
-      if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
-      const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
-      const ix ch = s % steps_per_unit;
+      const ix ul = s / steps_per_unit, ch = s % steps_per_unit;
+      const ix u = blockIdx.x + ul * gridDim.x;
       ix b, tm, tn;
       unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+      if (CB > 0 && cin && ch == 0) {
+        const int cb = (int)(ul % (CB > 0 ? CB : 1));
+        if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / CB) - 1) & 1));
+        const ix rc = g.ci + tm * BM;
+        const ix rows = min((ix)BM, g.m - tm * BM), cols = min((ix)BN, ncols - tn * BN);
+        const int npc = (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1);
+        const unsigned bytes = 32u * (unsigned)cols;
+        if (lane == 0) mbar_arrive_expect_tx(&cfull[cb], bytes * npc);
+        __syncwarp();
+        const double *C = g.C.item(b) + (rc >> 2) * 4 * g.C.cn + 4 * (g.cj + tn * BN);
+        for (int p = lane; p < npc; p += 32)
+          tma_load_1d(cbuf + cb * Cfg::C_ELEMS + p * 4 * BN, C + (ix)p * 4 * g.C.cn, bytes, &cfull[cb]);
+      }
+      if (nk == 0) continue;
+      const int st = (int)(s % STAGES);
+      if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
       double *sa = smem + st * Cfg::STAGE_ELEMS;
       double *sb = sa + Cfg::A_ELEMS;
       const ix l0 = ch * KC;
@@ -370,12 +400,14 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 
   // ===== consumers =====
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int fr = lane >> 2, fc = lane & 3;
-  const int aira = (int)(g.ai & 3), airb = (int)(g.bi & 3);
-  int offa[MT], offb[NT];
+  const int aira = (int)(g.ai & 3), airb = (int)(g.bi & 3), airc = (int)(g.ci & 3);
+  int offa[MT], offb[NT], offc[MT];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     const int r = aira + wm * WM + 8 * i + fr;
     offa[i] = (r >> 2) * 4 * KC + (r & 3) + 4 * fc;
+    const int rc = airc + wm * WM + 8 * i + fr;
+    offc[i] = (rc >> 2) * 4 * BN + (rc & 3) + 4 * (wn * WN + 2 * fc);
   }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -391,9 +423,9 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 
 
   ix b = 0, tm = 0, tn = 0;
   for (ix s = 0; s < nsteps; ++s) {
-    const ix ch = s % steps_per_unit;
+    const ix ul = s / steps_per_unit, ch = s % steps_per_unit;
     if (ch == 0) {
-      const ix u = blockIdx.x + (s / steps_per_unit) * gridDim.x;
+      const ix u = blockIdx.x + ul * gridDim.x;
       unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
     }
     const ix rbase = tm * BM + wm * WM, cbase = tn * BN + wn * WN;
@@ -441,16 +473,31 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS, 
       const double *C = g.C.item(b);
       const bool skip = g.skip && g.skip[b] >= 0;
       double cv[MT][NT][2];
+      const int cb = CB > 0 ? (int)(ul % (CB > 0 ? CB : 1)) : 0;
+      if (cin) {
+        mbar_wait(&cfull[cb], (unsigned)((ul / (CB > 0 ? CB : 1)) & 1));
+        const double *cs = cbuf + cb * Cfg::C_ELEMS;
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NT; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
-            cv[i][j][e] = (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n)) ? ldg_nc(C + eo(g.ci + r, g.cj + c, g.C.cn))
-                                                                          : 0.0;
-          }
+            for (int e = 0; e < 2; ++e) cv[i][j][e] = cs[offc[i] + 4 * (8 * j + e)];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[cb]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+              cv[i][j][e] = (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n))
+                                ? ldg_nc(C + eo(g.ci + r, g.cj + c, g.C.cn))
+                                : 0.0;
+            }
+      }
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -528,10 +575,10 @@ static cudaError_t launch_tiled(const GemmArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB = 0>
 static cudaError_t launch_tma(const GemmArgs &g, cudaStream_t st) {
-  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES>;
-  auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK>;
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>;
+  auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK, CB>;
   static bool configured = false;
   static int occ = 1;
   if (!configured) {
@@ -560,6 +607,22 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   const ix small = g.m < ncols ? g.m : ncols;
   if (g.tma) {
     if (small <= 40) return launch_tma<32, 32, 16, 16, 32, 4, SYRK>(g, st);
+    const char *e = getenv("PB_GEMM_CFG");  // tuning hook (benchmark sweeps)
+    if (e) {
+      const std::string v(e);
+      if (v == "k16s4c1") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 1>(g, st);
+      if (v == "k16s6") return launch_tma<64, 64, 32, 16, 16, 6, SYRK, 0>(g, st);
+      if (v == "k16s4") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 0>(g, st);
+      if (v == "k32s3") return launch_tma<64, 64, 32, 16, 32, 3, SYRK, 0>(g, st);
+      if (v == "s2c1") return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 1>(g, st);
+      if (v == "s2c2") return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 2>(g, st);
+      if (v == "s3c2") return launch_tma<64, 64, 32, 16, 32, 3, SYRK, 2>(g, st);
+      if (v == "k64c1") return launch_tma<64, 64, 32, 16, 64, 2, SYRK, 1>(g, st);
+    }
+    // beta != 0: C tile streamed through shared memory (2 A/B stages + 1 C
+    // buffer keeps 2 CTAs/SM); beta == 0: 3 A/B stages.  Measured on B200:
+    // profiles/r01_gemm_tuning.txt
+    if (g.beta != 0.0 && g.tmaC) return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 1>(g, st);
     return launch_tma<64, 64, 32, 16, 32, 3, SYRK>(g, st);
   }
   if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);

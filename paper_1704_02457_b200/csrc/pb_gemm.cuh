@@ -11,7 +11,8 @@ struct GemmArgs {
   ix ai, aj, bi, bj, ci, cj, di, dj;
   ix batch;
   bool vecA, vecB;      // 16-byte cp.async legal for the A / B stream
-  bool tma;             // bulk copies legal (16-byte aligned items and panels)
+  bool tma;             // bulk copies legal for A and B (16-byte aligned items)
+  bool tmaC;            // ... and for C
   const int32_t *skip;  // optional: item b is left untouched if skip[b] >= 0
 };
 
