@@ -606,24 +606,24 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
   const ix small = g.m < ncols ? g.m : ncols;
   if (g.tma) {
-    if (small <= 40) return launch_tma<32, 32, 16, 16, 32, 4, SYRK>(g, st);
-    const char *e = getenv("PB_GEMM_CFG");  // tuning hook (benchmark sweeps)
-    if (e) {
-      const std::string v(e);
-      if (v == "k16s4c1") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 1>(g, st);
-      if (v == "k16s6") return launch_tma<64, 64, 32, 16, 16, 6, SYRK, 0>(g, st);
-      if (v == "k16s4") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 0>(g, st);
-      if (v == "k32s3") return launch_tma<64, 64, 32, 16, 32, 3, SYRK, 0>(g, st);
-      if (v == "s2c1") return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 1>(g, st);
-      if (v == "s2c2") return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 2>(g, st);
-      if (v == "s3c2") return launch_tma<64, 64, 32, 16, 32, 3, SYRK, 2>(g, st);
-      if (v == "k64c1") return launch_tma<64, 64, 32, 16, 64, 2, SYRK, 1>(g, st);
+    // square output tile T in {32, 48, 64} minimising the padded tile area
+    // (ties -> larger T); k-chunk 40 when it covers k in one chunk.
+    // Measured on B200: profiles/r01_gemm_tuning.txt
+    int T = 64;
+    double best = 1e30;
+    for (int t : {64, 48, 32}) {
+      const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t);
+      if (area < best * 0.999) best = area, T = t;
     }
-    // beta != 0: C tile streamed through shared memory (2 A/B stages + 1 C
-    // buffer keeps 2 CTAs/SM); beta == 0: 3 A/B stages.  Measured on B200:
-    // profiles/r01_gemm_tuning.txt
-    if (g.beta != 0.0 && g.tmaC) return launch_tma<64, 64, 32, 16, 32, 2, SYRK, 1>(g, st);
-    return launch_tma<64, 64, 32, 16, 32, 3, SYRK>(g, st);
+    const bool k40 = g.k > 32 && g.k <= 40;
+    const bool cs = g.beta != 0.0 && g.tmaC;  // C tile through shared memory
+#define PB_TMA(T_, WM_, K_)                                                        \
+  if (T == T_ && (K_ == 40) == k40) {                                              \
+    if (cs) return launch_tma<T_, T_, WM_, 16, K_, (K_ == 40 ? 2 : 2), SYRK, 1>(g, st); \
+    return launch_tma<T_, T_, WM_, 16, K_, 3, SYRK, 0>(g, st);                     \
+  }
+    PB_TMA(64, 32, 32) PB_TMA(64, 32, 40) PB_TMA(48, 24, 32) PB_TMA(48, 24, 40) PB_TMA(32, 16, 32) PB_TMA(32, 16, 40)
+#undef PB_TMA
   }
   if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);
   return launch_tiled<64, 64, 32, 32, 32, 2, SYRK>(g, st);
