@@ -125,6 +125,17 @@ int pb_dunpack(int m, int n, const pb_dmat_batch *sS, int si, int sj,
 int pb_dgecp(int m, int n, const pb_dmat_batch *sS, int si, int sj,
              const pb_dmat_batch *sD, int di, int dj, void *stream);
 
+/* Fused Config-5 chain: for every problem run
+ * `stages` times  W = BAt P^T; lower(M) = W BAt^T + RQ; F = chol(M);
+ * K = -F21 F11^{-T}; P = F22 F22^T  -- the composition of pb_dgemm_nt,
+ * pb_dsyrk_ln, pb_dpotrf_l, pb_dtrsm_rltn, pb_dgemm_nt -- in one persistent
+ * kernel with each problem resident in shared memory.  BAt: (nx+nu) x nx,
+ * RQ: (nx+nu) x (nx+nu) (lower read), P: nx x nx (in: P_N, out: P_0),
+ * K: nx x nu (last stage).  nx in {8,16,24,32,48,64}, nu == 8.
+ * info[b] = -1, or stage*1000 + first bad pivot. */
+int pb_driccati_chain(int nx, int nu, int stages, const pb_dmat_batch *sBAt, const pb_dmat_batch *sRQ,
+                      const pb_dmat_batch *sP, const pb_dmat_batch *sK, int32_t *info, void *stream);
+
 /* Number of kernels this thread has launched through the ABI since the
  * last reset (bench.py's gpu_launches evidence). */
 int64_t pb_launch_count(int reset);

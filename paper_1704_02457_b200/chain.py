@@ -19,9 +19,11 @@ different, out-of-scope composition.  Problems are time-invariant
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
-from . import level3
+from . import _native, level3
 from .matstore import allocate_panel_batch
 
 
@@ -66,6 +68,22 @@ class RiccatiChain:
 
     def replay(self):
         self.graph.replay()
+
+    def fused_supported(self):
+        return self.nu == 8 and self.nx in (8, 16, 24, 32, 48, 64)
+
+    def run_fused(self, stages):
+        """All `stages` in one persistent kernel (pb_driccati_chain): every
+        problem stays resident in shared memory; P <- P_0, K <- last stage's K.
+        Returns the per-problem info tensor (-1 ok, else stage*1000 + pivot)."""
+        if not self.fused_supported():
+            raise NotImplementedError("fused chain needs nu == 8 and nx in {8,16,24,32,48,64}")
+        info = torch.empty(self.batch, dtype=torch.int32, device=self.P.device)
+        d = [x.descriptor() for x in (self.BAt, self.RQ, self.P, self.K)]
+        stream = ctypes.c_void_p(torch.cuda.current_stream(self.P.device).cuda_stream)
+        _native.call("pb_driccati_chain", self.nx, self.nu, stages, *[ctypes.byref(x) for x in d],
+                     ctypes.c_void_p(info.data_ptr()), stream)
+        return info
 
 
 def flops_per_stage(nx, nu):

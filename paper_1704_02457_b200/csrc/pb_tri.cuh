@@ -1,0 +1,123 @@
+// Device building blocks shared by the factorization kernels (pb_factor.cu)
+// and the fused Riccati chain (pb_chain.cu): the compact tri-panel shared
+// memory layout, 8x8 tile fragments, the in-register diagonal Cholesky
+// factor and the DMMA triangular solve through inverted diagonal blocks.
+#pragma once
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+// ---- compact tri-panel layout ---------------------------------------------
+// Row group g (rows 8g..8g+7, panels 2g and 2g+1) stores columns
+// [0, w_g), w_g = min(8g+8, cn8), cn8 = round_up(n, 8).
+struct Tri {
+  int gn;   // column groups = cn8 / 8
+  int cn8;
+  __device__ __forceinline__ int width(int g) const { return g < gn ? 8 * g + 8 : cn8; }
+  __device__ __forceinline__ int group_off(int g) const {
+    return g < gn ? 32 * g * (g + 1) : 32 * gn * (gn + 1) + 8 * (g - gn) * cn8;
+  }
+  // element (r, c) with c < width(r/8)
+  __device__ __forceinline__ int off(int r, int c) const {
+    const int g = r >> 3;
+    return group_off(g) + ((r >> 2) & 1) * 4 * width(g) + 4 * c + (r & 3);
+  }
+  static __host__ __device__ ix size(ix m, ix n) {
+    const ix cn8 = (n + 7) / 8 * 8, gn = cn8 / 8, gm = (m + 7) / 8;
+    return gm <= gn ? 32 * gm * (gm + 1) : 32 * gn * (gn + 1) + 8 * (gm - gn) * cn8;
+  }
+};
+
+// Fragment offset of (row group g, k-step kk) for lane: rows 8g+(lane>>2),
+// col 4kk+(lane&3).
+__device__ __forceinline__ int tri_frag(const Tri &t, int g, int kk, int lane) {
+  return t.group_off(g) + (lane >> 4) * 4 * t.width(g) + 16 * kk + 4 * (lane & 3) + ((lane >> 2) & 3);
+}
+
+// In-register solve of an 8x8 accumulator tile x (fragment layout: lane
+// holds row lane>>2, cols 2(lane&3)+e) against the lower 8x8 diagonal
+// block L (shared, tri layout at rows/cols 8j..), x <- x * L^{-T}, with
+// reciprocals dinv (shared).  ncol = valid columns in the block.
+__device__ __forceinline__ void solve_tile_rt(double (&x)[2], const double *S, const Tri &t, int j,
+                                              const double *dinv, int ncol, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < ncol) {
+      const double inv = dinv[8 * j + c];
+      if (fc == (c >> 1)) x[c & 1] = __dmul_rn(x[c & 1], inv);
+      const double xc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c2 = 2 * fc + e;
+        if (c2 > c && c2 < ncol) x[e] = fma(-xc, S[t.off(8 * j + c2, 8 * j + c)], x[e]);
+      }
+    }
+  }
+}
+
+// Right-looking in-register Cholesky of the 8x8 diagonal tile (fragment
+// layout).  Returns the first failing column (d <= 0) or -1.  On return the
+// tile holds L for columns < the failing one; dinv_out[c] = 1/L[c,c].
+__device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double *dinv_out, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  int fail = -1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < ncol && fail < 0) {
+      const double d = __shfl_sync(0xffffffffu, x[c & 1], c * 4 + (c >> 1));
+      if (d <= 0.0) {
+        fail = c;
+      } else {
+        const double inv = rsqrt(d);  // 1/L[c,c] (<= 1 ulp), one MUFU + Newton
+        const double ljj = d * inv;
+        if (fc == (c >> 1)) {
+          if (fr == c) x[c & 1] = ljj;
+          else if (fr > c) x[c & 1] = __dmul_rn(x[c & 1], inv);
+        }
+        if (lane == 0) dinv_out[c] = inv;
+        const double lrc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
+        const double l0 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc) * 4 + (c >> 1));
+        const double l1 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc + 1) * 4 + (c >> 1));
+        if (2 * fc > c) x[0] = fma(-lrc, l0, x[0]);
+        if (2 * fc + 1 > c) x[1] = fma(-lrc, l1, x[1]);
+      }
+    }
+  }
+  return fail;
+}
+
+
+// W = L_jj^{-1} of the 8x8 diagonal block (rows/cols 8j..), written to Wp in
+// panel layout (element (n, k) at (n>>2)*32 + 4k + (n&3)) so that it is read
+// back as the B operand of an m8n8k4 MMA:  X * L_jj^{-T} = X * W^T.  Built by
+// solving the identity against L_jj in registers (one warp, 8 serial steps);
+// columns past ncol stay identity.
+__device__ __forceinline__ void build_inv_block(const double *S, const Tri &t, int j, const double *dinv, int ncol,
+                                                double *Wp, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  double x[2];
+  x[0] = (fr == 2 * fc) ? 1.0 : 0.0;
+  x[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
+  solve_tile_rt(x, S, t, j, dinv, ncol, lane);  // x = I * L^{-T}: x[r][c] = Linv[c][r]
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * fc + e, k = fr;
+    Wp[(n >> 2) * 32 + 4 * k + (n & 3)] = x[e];
+  }
+}
+
+// acc := X * W^T for an 8x8 tile X held in shared memory (tri layout, rows
+// 8g.., cols 8j..) and W from build_inv_block.
+__device__ __forceinline__ void apply_inv_block(double (&acc)[2], const double *S, const Tri &t, int g, int j,
+                                                const double *Wp, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  const int fa = tri_frag(t, g, 0, lane) + 32 * j;  // column block j starts at 4*8j
+  const int fb = (lane >> 4) * 32 + 4 * fc + (fr & 3);
+  acc[0] = acc[1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) dmma(acc, S[fa + 16 * kk], Wp[fb + 16 * kk]);
+}
+
+
+}  // namespace pb

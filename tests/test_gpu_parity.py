@@ -516,3 +516,24 @@ def test_riccati_chain_c5_vs_oracle_and_graph_replay():
     torch.cuda.synchronize()
     assert torch.equal(g.P.storage, ch.P.storage)
     assert torch.equal(g.K.storage, ch.K.storage)
+
+
+def test_riccati_chain_fused_kernel_vs_oracle():
+    """The fused persistent chain kernel (pb_driccati_chain) matches the oracle
+    chain and the per-stage batched path."""
+    from chain_util import make_problems, oracle_chain, packed_inputs
+    from paper_1704_02457_b200.chain import RiccatiChain
+    for nb, nx, nu, N in [(16, 32, 8, 50), (7, 16, 8, 9), (5, 64, 8, 3)]:
+        A, B, Q, R = make_problems(nb, nx, nu, seed=nx)
+        BAt, RQ, P0 = packed_inputs(A, B, Q, R)
+        ch = RiccatiChain(nb, nx, nu)
+        pack.pack_array_into(torch.from_numpy(BAt).cuda(), ch.BAt)
+        pack.pack_array_into(torch.from_numpy(RQ).cuda(), ch.RQ)
+        pack.pack_array_into(torch.from_numpy(P0).cuda(), ch.P)
+        info = ch.run_fused(N)
+        assert int((info >= 0).sum()) == 0
+        P = pack.panel_to_array(ch.P).cpu().numpy()
+        K = pack.panel_to_array(ch.K).cpu().numpy()
+        Pw, Kw = oracle_chain(BAt, RQ, P0, nx, nu, N)
+        fp_close(P, Pw, nx + nu, f"fused P nx={nx}")
+        fp_close(K, Kw, nx + nu, f"fused K nx={nx}")
