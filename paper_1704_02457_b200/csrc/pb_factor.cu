@@ -348,8 +348,10 @@ cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
   const ix gn = (g.n + 7) / 8;
   // compile-time shaped instances for the common (benchmark) sizes
-  if (gm == 4 && gn == 4) return launch_potrf<1, 4, true, 4, 4>(g, st);
-  if (gm == 8 && gn == 8) return launch_potrf<4, 2, true, 8, 8>(g, st);
+  // measured on B200 (profiles/r01_potrf_team_tuning.txt): more, smaller
+  // teams without double buffering win where the diagonal chain dominates
+  if (gm == 4 && gn == 4) return launch_potrf<1, 4, false, 4, 4>(g, st);
+  if (gm == 8 && gn == 8) return launch_potrf<2, 4, false, 8, 8>(g, st);
   if (gm <= 2) return db ? launch_potrf<1, 2, true>(g, st) : launch_potrf<1, 2, false>(g, st);
   if (gm <= 4) return db ? launch_potrf<1, 4, true>(g, st) : launch_potrf<1, 4, false>(g, st);
   if (gm <= 8) return db ? launch_potrf<4, 2, true>(g, st) : launch_potrf<4, 2, false>(g, st);

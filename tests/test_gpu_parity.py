@@ -537,3 +537,55 @@ def test_riccati_chain_fused_kernel_vs_oracle():
         Pw, Kw = oracle_chain(BAt, RQ, P0, nx, nu, N)
         fp_close(P, Pw, nx + nu, f"fused P nx={nx}")
         fp_close(K, Kw, nx + nu, f"fused K nx={nx}")
+
+
+def test_composite_kkt_schur_and_block_tridiag_vs_oracle():
+    """§8f row 2 composites (apps.py:46-59, 268-293) batched on the GPU vs the
+    same compositions on the oracle."""
+    from paper_1704_02457_b200 import composite
+    rng = np.random.default_rng(42)
+    nb, n, m = 9, 20, 7
+    H = spd_batch(rng, nb, n)
+    A = rng.uniform(-1, 1, (nb, m, n))
+    f = composite.kkt_schur_factor(n, m, pack.panel_from_array(H), pack.panel_from_array(A))
+    hH, hA = O.HostBatch(nb, n, n), O.HostBatch(nb, m, n)
+    hH.set_window(0, 0, H)
+    hA.set_window(0, 0, A)
+    lh, mm, sig, ls = O.HostBatch(nb, n, n), O.HostBatch(nb, m, n), O.HostBatch(nb, m, m), O.HostBatch(nb, m, m)
+    O.potrf_l(n, hH, 0, 0, lh, 0, 0)
+    O.trsm_rltn(m, n, 1.0, lh, 0, 0, hA, 0, 0, mm, 0, 0)
+    O.syrk_ln(m, n, 1.0, mm, 0, 0, mm, 0, 0, 0.0, sig, 0, 0, sig, 0, 0)
+    O.potrf_l(m, sig, 0, 0, ls, 0, 0)
+    fp_close(np.tril(pack.panel_to_array(f.L_H).cpu().numpy()), np.tril(lh.window(0, 0, n, n)), n, "L_H")
+    fp_close(pack.panel_to_array(f.M).cpu().numpy(), mm.window(0, 0, m, n), n, "M")
+    fp_close(np.tril(pack.panel_to_array(f.L_S).cpu().numpy()), np.tril(ls.window(0, 0, m, m)), n, "L_S")
+    # block tridiagonal, N blocks of nx
+    N, nx = 6, 12
+    D = [spd_batch(rng, nb, nx, shift=4 * nx) for _ in range(N)]
+    E = [rng.uniform(-1, 1, (nb, nx, nx)) for _ in range(N - 1)]
+    bt = composite.block_tridiag_chol_factor(N, [pack.panel_from_array(x) for x in D],
+                                             [pack.panel_from_array(x) for x in E])
+    hd = O.HostBatch(nb, nx, nx)
+    hd.set_window(0, 0, D[0])
+    Ld = O.HostBatch(nb, nx, nx)
+    O.potrf_l(nx, hd, 0, 0, Ld, 0, 0)
+    for i in range(1, N):
+        he = O.HostBatch(nb, nx, nx)
+        he.set_window(0, 0, E[i - 1])
+        Lo = O.HostBatch(nb, nx, nx)
+        O.trsm_rltn(nx, nx, 1.0, Ld, 0, 0, he, 0, 0, Lo, 0, 0)
+        fp_close(pack.panel_to_array(bt.offdiag[i - 1]).cpu().numpy(), Lo.window(0, 0, nx, nx), nx, f"off {i}")
+        w = O.HostBatch(nb, nx, nx)
+        w.set_window(0, 0, D[i])
+        O.syrk_ln(nx, nx, -1.0, Lo, 0, 0, Lo, 0, 0, 1.0, w, 0, 0, w, 0, 0)
+        Ld = O.HostBatch(nb, nx, nx)
+        O.potrf_l(nx, w, 0, 0, Ld, 0, 0)
+        fp_close(np.tril(pack.panel_to_array(bt.diag[i]).cpu().numpy()), np.tril(Ld.window(0, 0, nx, nx)), nx,
+                 f"diag {i}")
+    # failure message carries the block index like the reference
+    bad = [x.copy() for x in D]
+    bad[0][3, 2, 2] = -1e3
+    with pytest.raises(pb.NotPositiveDefiniteError, match="block 0") as ei:
+        composite.block_tridiag_chol_factor(N, [pack.panel_from_array(x) for x in bad],
+                                            [pack.panel_from_array(x) for x in E])
+    assert ei.value.batch_index == 3 and ei.value.index == 2
