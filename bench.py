@@ -400,9 +400,36 @@ def run_ours(args):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
+        if args.csv:
+            emit_csv(csv_rows(points, pts), args.csv)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def csv_rows(points, pts, impl="b200"):
+    """Rows in the reference's sweep CSV schema (bench.py:436-462):
+    routine,impl,m,n,k,seconds,gflops -- seconds = per-call time amortised
+    over the batch (so rows compare 1:1 with the reference's per-call rows)."""
+    rows = []
+    for p, pt in zip(points, pts):
+        if pt.op == "potrf_l":
+            m = n = k = pt.n
+        elif pt.op == "riccati":
+            m, n, k = pt.m, pt.n, pt.k
+        else:
+            m, n, k = pt.m, pt.n, pt.k
+        sec = p["ms"] / 1e3 / max(1, p["items"])
+        rows.append((pt.op, impl, m, n, k, sec, p["gflops"]))
+    return rows
+
+
+def emit_csv(rows, path):
+    """Write rows sorted by (routine, impl, m) with 17 significant digits."""
+    with open(path, "w") as fh:
+        fh.write("routine,impl,m,n,k,seconds,gflops\n")
+        for r in sorted(rows, key=lambda r: (r[0], r[1], r[2])):
+            fh.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.17g},{r[6]:.17g}\n")
 
 
 def traffic_from_profile(pt):
@@ -668,6 +695,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=14.0)
     ap.add_argument("--ref-seconds", type=float, default=7.0)
+    ap.add_argument("--csv", default=None, help="also write per-point rows in the reference's sweep CSV schema")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -128,3 +128,22 @@ def test_colbatch_roundtrip_host_side():
     assert cb.lda == 3 and cb.data.shape == (2, 12)
     assert float(cb.data[1, 0 + 2 * 3]) == arr[1, 0, 2]
     assert np.array_equal(cb.to_array().numpy(), arr)
+
+
+def test_bench_csv_matches_reference_schema(tmp_path):
+    """bench.py --csv writes the reference's sweep CSV (bench.py:436-462):
+    header, sorted rows, 17 significant digits, parseable by its reader."""
+    import sys
+    sys.path.insert(0, REPO)
+    import bench
+    pts, _ = bench.config_points("c2")
+    points = [{"ms": 1.0 + i, "items": 1000 * (i + 1), "gflops": 10.0 * (i + 1)} for i in range(len(pts))]
+    path = tmp_path / "sweep.csv"
+    bench.emit_csv(bench.csv_rows(points, pts), str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == "routine,impl,m,n,k,seconds,gflops"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert len(rows) == len(pts)
+    ms = [int(r[2]) for r in rows]
+    assert ms == sorted(ms) and rows[0][0] == "potrf_l" and rows[0][1] == "b200"
+    assert float(rows[0][5]) == (1.0 / 1e3) / 1000 and float(rows[-1][6]) == 70.0
