@@ -514,6 +514,138 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
 }
 
 // ---------------------------------------------------------------------------
+// gemm_item: one THREAD per item for m, n <= 4 (one panel), k <= 16 -- the
+// smallest C3 points are pure HBM streaming, so the kernel mirrors the
+// tiny-potrf design: persistent CTAs, a 2-stage cp.async ring of the
+// items' A/B(/C) panel runs (16-byte pieces, coalesced across the warp),
+// the product in registers (FMA), coalesced 16-byte stores of D's window.
+
+template <int KMAX>
+struct ItemCfg {
+  static constexpr int NTH = 128, ITEMS = NTH;
+  static constexpr int STRIDE = 3 * 4 * KMAX + 2;  // A, B (4 x KMAX each) + C (4 x 4 <= 4 x KMAX), padded
+  static constexpr size_t SMEM = sizeof(double) * 2 * ITEMS * STRIDE;
+};
+
+template <int KMAX, bool SYRK>
+__global__ void __launch_bounds__(128) gemm_item_kernel(GemmArgs g) {
+  using Cfg = ItemCfg<KMAX>;
+  constexpr int ITEMS = Cfg::ITEMS, NTH = Cfg::NTH, STRIDE = Cfg::STRIDE;
+  extern __shared__ __align__(128) double smem[];
+  const int tid = threadIdx.x;
+  const int m = (int)g.m, n = (int)g.n, k = (int)g.k;
+  const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
+  const bool rc = g.beta != 0.0, ab = g.alpha != 0.0;
+  // pieces per item: A 2k, B 2k, C 2n (16 bytes each)
+  const int pa = ab ? 2 * k : 0, pbb = ab ? 2 * k : 0, pc = rc ? 2 * n : 0;
+  const int pieces = pa + pbb + pc;
+
+  auto issue = [&](ix rd, int buf) {
+    double *S = smem + buf * ITEMS * STRIDE;
+    const ix b0 = rd * ITEMS;
+    for (int q = tid; q < ITEMS * pieces; q += NTH) {
+      const int it = q / pieces, w = q - it * pieces;
+      const ix b = b0 + it;
+      const bool ok = b < g.batch;
+      const double *src;
+      int dst;
+      if (w < pa) {
+        src = g.A.item(b) + eo(g.ai, g.aj + (w >> 1), g.A.cn) + 2 * (w & 1);
+        dst = 2 * w;
+      } else if (w < pa + pbb) {
+        const int v = w - pa;
+        src = g.B.item(b) + eo(g.bi, g.bj + (v >> 1), g.B.cn) + 2 * (v & 1);
+        dst = 4 * KMAX + 2 * v;
+      } else {
+        const int v = w - pa - pbb;
+        src = g.C.item(b) + eo(g.ci, g.cj + (v >> 1), g.C.cn) + 2 * (v & 1);
+        dst = 8 * KMAX + 2 * v;
+      }
+      cp_async16(S + it * STRIDE + dst, ok ? src : g.D.p, ok ? 16 : 0);
+    }
+  };
+
+  if (blockIdx.x < nrounds) issue(blockIdx.x, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf ^= 1) {
+    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double *S = smem + buf * ITEMS * STRIDE + tid * STRIDE;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    if (ab) {
+#pragma unroll
+      for (int l = 0; l < KMAX; ++l) {
+        if (l < k) {
+          const double2 a01 = *reinterpret_cast<const double2 *>(S + 4 * l);
+          const double2 a23 = *reinterpret_cast<const double2 *>(S + 4 * l + 2);
+          const double2 b01 = *reinterpret_cast<const double2 *>(S + 4 * KMAX + 4 * l);
+          const double2 b23 = *reinterpret_cast<const double2 *>(S + 4 * KMAX + 4 * l + 2);
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+      }
+    }
+    // epilogue into the same slot (A's area), then coalesced stores
+    __syncthreads();
+    const ix b = rd * ITEMS + tid;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double cv = rc ? S[8 * KMAX + 4 * j + i] : 0.0;
+        S[4 * j + i] = (SYRK && (i >> 2) == (j >> 2)) ? syrk_diag_rule(g.alpha, acc[i][j], g.beta, cv)
+                                                       : store_rule(g.alpha, acc[i][j], g.beta, cv);
+      }
+    __syncthreads();
+    const ix b0 = rd * ITEMS;
+    for (int q = tid; q < ITEMS * 2 * n; q += NTH) {
+      const int it = q / (2 * n), w = q - it * 2 * n;
+      const ix bb = b0 + it;
+      if (bb >= g.batch || (g.skip && g.skip[bb] >= 0)) continue;
+      const int col = w >> 1, h = w & 1;
+      const double *src = smem + buf * ITEMS * STRIDE + it * STRIDE + 4 * col + 2 * h;
+      double *dst = g.D.item(bb) + eo(g.di, g.dj + col, g.D.cn) + 2 * h;
+      const int r0 = 2 * h;
+      const bool w0 = r0 < m && (!SYRK || r0 >= col), w1 = r0 + 1 < m && (!SYRK || r0 + 1 >= col);
+      if (w0 && w1) *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(src);
+      else if (w0) dst[0] = src[0];
+      else if (w1) dst[1] = src[1];
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+template <int KMAX, bool SYRK>
+static cudaError_t launch_item(const GemmArgs &g, cudaStream_t st) {
+  using Cfg = ItemCfg<KMAX>;
+  auto kern = gemm_item_kernel<KMAX, SYRK>;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTH, Cfg::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > rounds) grid = rounds;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, Cfg::NTH, Cfg::SMEM, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host dispatch
 
 static int g_num_sms = 0;
@@ -603,6 +735,14 @@ template <bool SYRK>
 static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   const ix ncols = SYRK ? g.m : g.n;
   const ix big = g.m > ncols ? g.m : ncols;
+  // one thread per item: one-panel windows (rows in a single aligned panel)
+  // with 16-byte aligned item storage
+  const bool one_panel = (g.ai & 3) == 0 && (g.bi & 3) == 0 && (g.ci & 3) == 0 && (g.di & 3) == 0 && g.tma && g.tmaC &&
+                         ((uintptr_t)g.D.p & 15) == 0 && (g.D.stride & 1) == 0;
+  if (big <= 4 && one_panel) {
+    if (g.k <= 4) return launch_item<4, SYRK>(g, st);
+    if (g.k <= 16) return launch_item<16, SYRK>(g, st);
+  }
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
   const ix small = g.m < ncols ? g.m : ncols;
   if (g.tma) {
