@@ -11,8 +11,8 @@
 //    the masked stores of the results are fully coalesced;
 //  * n <= 8: one thread owns one item, entirely in registers;
 //    9 <= n <= 16: a quad of threads owns one item, thread q owning panel q
-//    (rows 4q..4q+3), left-looking over 4-column blocks with the block row
-//    broadcast through warp shuffles.
+//    (rows 4q..4q+3), left-looking over 4-column blocks, computed in place
+//    in the staged shared-memory copy (block rows read back by broadcast).
 //
 // Arithmetic follows the reference's per-element operation order exactly
 // (potrf_drv ccore.pyx:877-905, _kpotrf_core :404-438, _trsm_rltn_core
@@ -129,44 +129,54 @@ __device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], do
   return -1;
 }
 
-// One item, a quad of threads (9 <= n <= 16): thread q owns panel q.
-// Left-looking over column blocks s; per element the operation order is
-// the reference's (see file header), so results are bit-identical.  The
-// quad stays converged around every shuffle; only the diagonal factor
-// (no shuffles) runs on thread s alone.
+// One item, a quad of threads (9 <= n <= 16), computed IN SHARED MEMORY:
+// thread q owns panel q (rows 4q..4q+3) of the staged lower prefix; the
+// block row s it downdates against is read back from shared memory
+// (broadcast), so no register copy of the item is needed (few registers,
+// many warps per SM).  Left-looking over 4-column blocks; per element the
+// reference's operation order, IEEE sqrt/div, no FMA: bit-identical.
 template <int N>
-__device__ __forceinline__ int factor_t4(double (&L)[4][N], double *dinv, int q, int qbase) {
-  constexpr int NP = SmallCfg<N>::NP;
+__device__ __forceinline__ int factor_t4s(double *Si, double *dinv, int q, volatile int *flag) {
+  using Cfg = SmallCfg<N>;
+  constexpr int NP = Cfg::NP;
   int fail = -1;
+  const bool own = q < NP;
+  double *Lq = Si + (own ? Cfg::poff(q < NP ? q : 0) : 0);  // element (r, l) at Lq[4l + r]
+  if (q == 0) *flag = -1;
+  __syncwarp();
 #pragma unroll
   for (int s = 0; s < NP; ++s) {
     const int ns = N - 4 * s < 4 ? N - 4 * s : 4;
-    const bool alive = fail < 0;
+    const double *Ls = Si + Cfg::poff(s);  // block row s: element (c, l) at Ls[4l + c]
+    const bool act = own && q >= s && fail < 0;
     double acc[4][4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[c][r] = 0.0;
-    // downdate with block row s (broadcast from thread s), l ascending
+    if (act) {
 #pragma unroll
-    for (int l = 0; l < 4 * s; ++l) {
+      for (int l = 0; l < 4 * s; ++l) {
+        const double2 lo = *reinterpret_cast<const double2 *>(Lq + 4 * l);
+        const double2 hi = *reinterpret_cast<const double2 *>(Lq + 4 * l + 2);
+        const double lr[4] = {lo.x, lo.y, hi.x, hi.y};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < ns) {
-          const double v = __shfl_sync(0xffffffffu, L[c][l], qbase + s);
+        for (int c = 0; c < 4; ++c) {
+          if (c < ns) {
+            const double v = Ls[4 * l + c];
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acc[c][r] = dadd(acc[c][r], dmul(L[r][l], -v));
+            for (int r = 0; r < 4; ++r) acc[c][r] = dadd(acc[c][r], dmul(lr[r], -v));
+          }
         }
       }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (c < ns) acc[c][r] = dadd(acc[c][r], Lq[4 * (4 * s + c) + r]);
     }
-    // + C (still held in L for column block s)
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (c < ns) acc[c][r] = dadd(acc[c][r], L[r][4 * s + c]);
-    int f = -1;
-    if (q == s && alive) {
+    if (act && q == s) {
+      int f = -1;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (c < ns && f < 0) {
@@ -192,41 +202,36 @@ __device__ __forceinline__ int factor_t4(double (&L)[4][N], double *dinv, int q,
           }
         }
       }
-    }
-    const int fs = __shfl_sync(0xffffffffu, f, qbase + s);
-    if (alive && fs >= 0) fail = 4 * s + fs;
-    // the diagonal block's factor (strictly lower part) and reciprocals
-    double E[4][4], iv[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      iv[c] = c < ns ? __shfl_sync(0xffffffffu, acc[c][c], qbase + s) : 1.0;
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) E[c][t] = (t < c && c < ns) ? __shfl_sync(0xffffffffu, acc[t][c], qbase + s) : 0.0;
+        for (int r = 0; r < 4; ++r)
+          if (c < ns && r >= c && (f < 0 || c < f)) Lq[4 * (4 * s + c) + r] = acc[c][r];
+      if (f >= 0) *flag = 4 * s + f;
     }
-    if (q > s && fail < 0) {
+    __syncwarp();
+    fail = *flag;
+    if (act && q > s && fail < 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (c < ns) {
 #pragma unroll
           for (int t = 0; t < 4; ++t)
             if (t < c) {
+              const double e = Ls[4 * (4 * s + t) + c];
 #pragma unroll
-              for (int r = 0; r < 4; ++r) acc[c][r] = dsub(acc[c][r], dmul(acc[t][r], E[c][t]));
+              for (int r = 0; r < 4; ++r) acc[c][r] = dsub(acc[c][r], dmul(acc[t][r], e));
             }
-          // reciprocal = 1/L[c][c] exactly as the factor stored it
-          const double inv = __ddiv_rn(1.0, iv[c]);
+          const double inv = dinv[4 * s + c];
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acc[c][r] = dmul(acc[c][r], inv);
+          for (int r = 0; r < 4; ++r) {
+            acc[c][r] = dmul(acc[c][r], inv);
+            Lq[4 * (4 * s + c) + r] = acc[c][r];
+          }
         }
       }
     }
-    if ((q >= s) && alive) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (c < ns) L[r][4 * s + c] = acc[c][r];
-    }
+    __syncwarp();
   }
   return fail;
 }
@@ -315,33 +320,7 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
             *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c + 2) = make_double2(L[4 * p + 2][c], L[4 * p + 3][c]);
           }
     } else {
-      double L[4][N];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < N; ++c) L[r][c] = 0.0;
-#pragma unroll
-      for (int p = 0; p < NP; ++p)
-        if (p == q) {
-#pragma unroll
-          for (int c = 0; c < N; ++c)
-            if (c < Cfg::cols(p)) {
-              const double2 lo = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c);
-              const double2 hi = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c + 2);
-              L[0][c] = lo.x, L[1][c] = lo.y, L[2][c] = hi.x, L[3][c] = hi.y;
-            }
-        }
-      fail = factor_t4<N>(L, di, q, (tid & 31) & ~(T - 1));
-#pragma unroll
-      for (int p = 0; p < NP; ++p)
-        if (p == q) {
-#pragma unroll
-          for (int c = 0; c < N; ++c)
-            if (c < Cfg::cols(p)) {
-              *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c) = make_double2(L[0][c], L[1][c]);
-              *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c + 2) = make_double2(L[2][c], L[3][c]);
-            }
-        }
+      fail = factor_t4s<N>(Si, di, q, (volatile int *)(sinfo + it));
     }
     const ix b0 = rd * ITEMS;
     if (q == 0) {
@@ -469,6 +448,9 @@ static cudaError_t launch_small_tuned(const PotrfArgs &g, cudaStream_t st) {
     if (v == "128x3") return launch_small<N, 128, 3>(g, st);
     if (v == "256x2") return launch_small<N, 256, 2>(g, st);
     if (v == "64x4") return launch_small<N, 64, 4>(g, st);
+    if (v == "128x1") return launch_small<N, 128, 1>(g, st);
+    if (v == "64x1") return launch_small<N, 64, 1>(g, st);
+    if (v == "256x1") return launch_small<N, 256, 1>(g, st);
   }
   return launch_small<N>(g, st);
 }
