@@ -51,7 +51,7 @@ __device__ __forceinline__ int full_off(int r, int c, int cn) { return (r >> 2) 
 template <int NXB, int TW>
 __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
   using Cfg = ChainCfg<NXB, TW>;
-  constexpr int NB = Cfg::NB, NS = Cfg::NS, NX = Cfg::NX, NU = Cfg::NU;
+  constexpr int NB = Cfg::NB, NS = Cfg::NS, NX = Cfg::NX;
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int team = warp / TW, tw = warp % TW;

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
       unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
       if (CB > 0 && cin && ch == 0) {
         const int cb = (int)(ul % (CB > 0 ? CB : 1));
-        if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / CB) - 1) & 1));
+        if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / (CB > 0 ? CB : 1)) - 1) & 1));
         const ix rc = g.ci + tm * BM;
         const ix rows = min((ix)BM, g.m - tm * BM), cols = min((ix)BN, ncols - tn * BN);
         const int npc = (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1);
@@ -597,7 +597,6 @@ __global__ void __launch_bounds__(128) gemm_item_kernel(GemmArgs g) {
     }
     // epilogue into the same slot (A's area), then coalesced stores
     __syncthreads();
-    const ix b = rd * ITEMS + tid;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
