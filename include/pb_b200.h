@@ -15,6 +15,10 @@
  *   pb_dpack_cm    <- ccore.kpack_cm      (ccore.pyx:718-723)
  *   pb_dunpack_cm  <- ccore.kunpack_cm    (ccore.pyx:734-739)
  *   pb_dgecp       <- ccore.kgecp         (ccore.pyx:677-682)
+ * and, for the next tier of callers:
+ *   pb_dgemm_nn       <- ccore.gemm_nn_drv    (ccore.pyx:774-801)
+ *   pb_dtrmm_rlnn     <- ccore.trmm_rlnn_drv  (ccore.pyx:834-852)
+ *   pb_dsyrk_potrf_ln <- ccore.syrk_potrf_drv (ccore.pyx:908-941)
  *
  * Conventions (mirroring the reference core):
  *   - caller owns every buffer; nothing here allocates device memory;
@@ -81,6 +85,22 @@ int pb_dsyrk_ln(int m, int k, double alpha,
                 const pb_dmat_batch *sC, int ci, int cj,
                 const pb_dmat_batch *sD, int di, int dj, void *stream);
 
+/* D = alpha*A*B + beta*C; A m x k, B k x n (level3.py:101-117,
+ * gemm_nn_drv ccore.pyx:774-801).  Same special cases as pb_dgemm_nt. */
+int pb_dgemm_nn(int m, int n, int k, double alpha,
+                const pb_dmat_batch *sA, int ai, int aj,
+                const pb_dmat_batch *sB, int bi, int bj, double beta,
+                const pb_dmat_batch *sC, int ci, int cj,
+                const pb_dmat_batch *sD, int di, int dj, void *stream);
+
+/* D = alpha*B*A, A an n x n lower-triangular right factor (entries above
+ * its diagonal are never read), B and D m x n (level3.py:140-153,
+ * trmm_rlnn_drv ccore.pyx:834-852).  D = alpha*acc for every alpha. */
+int pb_dtrmm_rlnn(int m, int n, double alpha,
+                  const pb_dmat_batch *sA, int ai, int aj,
+                  const pb_dmat_batch *sB, int bi, int bj,
+                  const pb_dmat_batch *sD, int di, int dj, void *stream);
+
 /* D * A^T = alpha*B, A n x n lower non-unit, B and D m x n
  * (blasfeo_dtrsm_rltn).  Reciprocals of A's diagonal: use_dA != 0 reuses
  * sA->dA[aj .. aj+n) written by a factorization (level3.py:169-170);
@@ -103,6 +123,17 @@ int pb_dpotrf_l(int m, int n,
                 const pb_dmat_batch *sC, int ci, int cj,
                 const pb_dmat_batch *sD, int di, int dj,
                 int32_t *info, void *stream);
+
+/* D = chol(lower(C + A*B^T)), m x n with n <= m, A m x k, B n x k
+ * (level3.py:353-391, syrk_potrf_drv ccore.pyx:908-941): the product goes
+ * to a stream-ordered workspace, then pb_dpotrf_l's rules apply to it
+ * (info, diag_inv, partial writes of a failed item). */
+int pb_dsyrk_potrf_ln(int m, int n, int k,
+                      const pb_dmat_batch *sA, int ai, int aj,
+                      const pb_dmat_batch *sB, int bi, int bj,
+                      const pb_dmat_batch *sC, int ci, int cj,
+                      const pb_dmat_batch *sD, int di, int dj,
+                      int32_t *info, void *stream);
 
 /* Column-major -> panel-major copy (kpack_cm): item b's source element
  * (i, j) is S[b*s_stride + i + j*lds]. */

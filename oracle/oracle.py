@@ -48,6 +48,7 @@ def lib():
         _lib.po_element_offset.restype = ctypes.c_int64
         _lib.po_memsize.restype = ctypes.c_int64
         _lib.po_potrf_l.restype = ctypes.c_int
+        _lib.po_syrk_potrf_ln.restype = ctypes.c_int
     return _lib
 
 
@@ -194,6 +195,58 @@ def potrf_l(m, C, ci, cj, D, di, dj, n=None):
             s = HostBatch(1, m, n)
             st = lib().po_potrf_l(_L(m), _L(n), C.ptr(cb), _L(ci), _L(cj), _L(C.cn), s.ptr(), _L(0), _L(0),
                                   _L(s.cn), D.dptr(b), _L(dj))
+            info[b] = st
+            if st < 0:
+                for j in range(n):
+                    for i in range(j, m):
+                        D.storage[b, element_offset(di + i, dj + j, D.cn)] = s.get(0, i, j)
+    ok = bool(np.all(info < 0))
+    if ok and di == dj:
+        D.diag_lo, D.diag_hi = dj, dj + n
+    else:
+        D.diag_lo = D.diag_hi = 0
+    return info
+
+
+def _item(X, b):
+    return X.ptr(b if X.batch > 1 else 0)
+
+
+def gemm_nn(m, n, k, alpha, A, ai, aj, B, bi, bj, beta, C, ci, cj, D, di, dj):
+    """level3.gemm_nn semantics (level3.py:101-117) per item."""
+    if m == 0 or n == 0:
+        return
+    for b in range(D.batch):
+        lib().po_gemm_nn(_L(m), _L(n), _L(k), _D(alpha), _item(A, b), _L(ai), _L(aj), _L(A.cn),
+                         _item(B, b), _L(bi), _L(bj), _L(B.cn), _D(beta), _item(C, b), _L(ci), _L(cj), _L(C.cn),
+                         D.ptr(b), _L(di), _L(dj), _L(D.cn))
+
+
+def trmm_rlnn(m, n, alpha, A, ai, aj, B, bi, bj, D, di, dj):
+    """level3.trmm_rlnn (level3.py:140-153): D = alpha * B * A, A lower n x n."""
+    if m == 0 or n == 0:
+        return
+    for b in range(D.batch):
+        lib().po_trmm_rlnn(_L(m), _L(n), _D(alpha), _item(A, b), _L(ai), _L(aj), _L(A.cn),
+                           _item(B, b), _L(bi), _L(bj), _L(B.cn), D.ptr(b), _L(di), _L(dj), _L(D.cn))
+
+
+def syrk_potrf_ln(m, k, A, ai, aj, B, bi, bj, C, ci, cj, D, di, dj, n=None):
+    """level3.syrk_potrf_ln (level3.py:353-391) -> info[batch]; unaligned
+    destinations go through a scratch matrix copied only on success."""
+    if n is None:
+        n = m
+    info = np.full(D.batch, -1, dtype=np.int32)
+    if n == 0:
+        return info
+    for b in range(D.batch):
+        args = (_L(m), _L(n), _L(k), _item(A, b), _L(ai), _L(aj), _L(A.cn), _item(B, b), _L(bi), _L(bj), _L(B.cn),
+                _item(C, b), _L(ci), _L(cj), _L(C.cn))
+        if di % 4 == 0:
+            info[b] = lib().po_syrk_potrf_ln(*args, D.ptr(b), _L(di), _L(dj), _L(D.cn), D.dptr(b), _L(dj))
+        else:
+            s = HostBatch(1, m, n)
+            st = lib().po_syrk_potrf_ln(*args, s.ptr(), _L(0), _L(0), _L(s.cn), D.dptr(b), _L(dj))
             info[b] = st
             if st < 0:
                 for j in range(n):

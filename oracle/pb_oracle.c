@@ -209,6 +209,103 @@ int po_potrf_l(ix m, ix n, const double *C, ix ci, ix cj, ix sdc,
   return -1;
 }
 
+
+/* ---- §8f next tier: gemm_nn, trmm_rlnn, syrk_potrf_ln ---------------- */
+
+/* gemm_nn: level3.py:101-117 + gemm_nn_drv ccore.pyx:774-801 (_acc_nn
+ * :130-245): D = alpha*A*B + beta*C, B read across panels; per element the
+ * sum starts at 0.0 and adds A[i,l]*B[l,j] for l ascending. */
+void po_gemm_nn(ix m, ix n, ix k, double alpha,
+                const double *A, ix ai, ix aj, ix sda,
+                const double *B, ix bi, ix bj, ix sdb, double beta,
+                const double *C, ix ci, ix cj, ix sdc,
+                double *D, ix di, ix dj, ix sdd) {
+  for (ix j = 0; j < n; ++j)
+    for (ix i = 0; i < m; ++i) {
+      double s = 0.0;
+      for (ix l = 0; l < k; ++l) s += A[eo(ai + i, aj + l, sda)] * B[eo(bi + l, bj + j, sdb)];
+      D[eo(di + i, dj + j, sdd)] = store_rule(alpha, s, beta, &C[eo(ci + i, cj + j, sdc)]);
+    }
+}
+
+/* trmm_rlnn: level3.py:140-153 + trmm_rlnn_drv ccore.pyx:834-852
+ * (_ktrmm_core :305-348): D = alpha*X*T, T n x n lower.  Column c of block
+ * jj = c & ~3 sums l = jj .. n-1 ascending; the triangle head uses 0.0 for
+ * T's strict upper (never read). */
+void po_trmm_rlnn(ix m, ix n, double alpha,
+                  const double *T, ix ti, ix tj, ix sdt,
+                  const double *X, ix xi, ix xj, ix sdx,
+                  double *D, ix di, ix dj, ix sdd) {
+  for (ix c = 0; c < n; ++c) {
+    const ix jj = c & ~(ix)3;
+    for (ix i = 0; i < m; ++i) {
+      double s = 0.0;
+      for (ix l = jj; l < n; ++l) s += X[eo(xi + i, xj + l, sdx)] * (l >= c ? T[eo(ti + l, tj + c, sdt)] : 0.0);
+      D[eo(di + i, dj + c, sdd)] = alpha * s;
+    }
+  }
+}
+
+/* syrk_potrf_ln: level3.py:353-391 + syrk_potrf_drv ccore.pyx:908-941:
+ * fused D = chol(lower(C + A*B^T)); per element the accumulator first adds
+ * A[i,l]*B[c,l] (l < k), then -L[i,l]*L[c,l] (l < jj), then C, then the
+ * in-tile updates.  n < m solves the trailing rows (tall variant). */
+int po_syrk_potrf_ln(ix m, ix n, ix k,
+                     const double *A, ix ai, ix aj, ix sda,
+                     const double *B, ix bi, ix bj, ix sdb,
+                     const double *C, ix ci, ix cj, ix sdc,
+                     double *D, ix di, ix dj, ix sdd, double *dinv, ix dio) {
+  for (ix ii = 0; ii < m; ii += 4) {
+    ix ms = m - ii < 4 ? m - ii : 4;
+    ix jmax = ii + 4 < n ? ii + 4 : n;
+    for (ix jj = 0; jj < jmax; jj += 4) {
+      ix ns = n - jj < 4 ? n - jj : 4;
+      double acc[4][4];
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = 0; r < ms; ++r) {
+          double s = 0.0;
+          for (ix l = 0; l < k; ++l) s += A[eo(ai + ii + r, aj + l, sda)] * B[eo(bi + jj + c, bj + l, sdb)];
+          for (ix l = 0; l < jj; ++l)
+            s += D[eo(di + ii + r, dj + l, sdd)] * (-D[eo(di + jj + c, dj + l, sdd)]);
+          acc[c][r] = s;
+        }
+      if (jj < ii) {
+        for (ix c = 0; c < ns; ++c) {
+          for (ix r = 0; r < ms; ++r) acc[c][r] += 1.0 * C[eo(ci + ii + r, cj + jj + c, sdc)];
+          for (ix t = 0; t < c; ++t) {
+            double e = D[eo(di + jj + c, dj + jj + t, sdd)];
+            for (ix r = 0; r < ms; ++r) acc[c][r] -= acc[t][r] * e;
+          }
+          double inv = dinv[dio + jj + c];
+          for (ix r = 0; r < ms; ++r) {
+            acc[c][r] *= inv;
+            D[eo(di + ii + r, dj + jj + c, sdd)] = acc[c][r];
+          }
+        }
+        continue;
+      }
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = 0; r < ms; ++r) acc[c][r] += C[eo(ci + ii + r, cj + jj + c, sdc)];
+      for (ix c = 0; c < ns; ++c) {
+        double d = acc[c][c];
+        if (d <= 0.0) return (int)(jj + c);
+        double ljj = sqrt(d);
+        double inv = 1.0 / ljj;
+        acc[c][c] = ljj;
+        dinv[dio + jj + c] = inv;
+        for (ix r = c + 1; r < ms; ++r) acc[c][r] *= inv;
+        for (ix c2 = c + 1; c2 < ns; ++c2) {
+          double lcj = acc[c][c2];
+          for (ix r = c2; r < ms; ++r) acc[c2][r] -= acc[c][r] * lcj;
+        }
+      }
+      for (ix c = 0; c < ns; ++c)
+        for (ix r = c; r < ms; ++r) D[eo(di + ii + r, dj + jj + c, sdd)] = acc[c][r];
+    }
+  }
+  return -1;
+}
+
 /* ---- naive column-major oracles: ccore.pyx:1109-1223 (o_*) ----
  * Independent of the panel machinery; used to cross-check the above. */
 void po_naive_potrf(ix m, const double *C, ix ldc, double *L, ix ldl) {

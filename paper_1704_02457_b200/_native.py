@@ -48,6 +48,9 @@ SIGNATURES = {
     "pb_dpack": (_i, [_i, _i, _v, _l, _l, _l, P, _i, _i, _v]),
     "pb_dunpack": (_i, [_i, _i, P, _i, _i, _v, _l, _l, _l, _v]),
     "pb_dgecp": (_i, [_i, _i, P, _i, _i, P, _i, _i, _v]),
+    "pb_dgemm_nn": (_i, [_i, _i, _i, _d, P, _i, _i, P, _i, _i, _d, P, _i, _i, P, _i, _i, _v]),
+    "pb_dtrmm_rlnn": (_i, [_i, _i, _d, P, _i, _i, P, _i, _i, P, _i, _i, _v]),
+    "pb_dsyrk_potrf_ln": (_i, [_i, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, _v, _v]),
     "pb_driccati_chain": (_i, [_i, _i, _i, P, P, P, P, _v, _v]),
 }
 

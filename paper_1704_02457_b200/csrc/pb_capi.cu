@@ -82,11 +82,13 @@ int64_t pb_launch_count(int reset) {
   return v;
 }
 
-static int gemm_common(bool syrk, int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj,
+static int gemm_common(int op, int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj,
                        const pb_dmat_batch *sB, int bi, int bj, double beta, const pb_dmat_batch *sC, int ci,
                        int cj, const pb_dmat_batch *sD, int di, int dj, void *stream, const int32_t *skip) {
   // positions: gemm (m1 n2 k3 alpha4 A5 ai6 aj7 B8 bi9 bj10 beta11 C12 ci13 cj14 D15 di16 dj17)
   //            syrk (m1 k2 alpha3 A4 ai5 aj6 B7 bi8 bj9 beta10 C11 ci12 cj13 D14 di15 dj16)
+  //            gemm_nn (as gemm_nt, B is k x n)
+  const bool syrk = op == 1, nn_b = op == 2;
   const int o = syrk ? -1 : 0;
   if (m < 0) return fail_arg(1, "negative size");
   if (!syrk && n < 0) return fail_arg(2, "negative size");
@@ -97,7 +99,7 @@ static int gemm_common(bool syrk, int m, int n, int k, double alpha, const pb_dm
   const int64_t nn = syrk ? m : n;
   int r;
   if ((r = check_mat(sA, 5 + o, ai, aj, m, k, batch, false))) return r;
-  if ((r = check_mat(sB, 8 + o, bi, bj, nn, k, batch, false))) return r;
+  if ((r = check_mat(sB, 8 + o, bi, bj, nn_b ? k : nn, nn_b ? nn : k, batch, false))) return r;
   if ((r = check_mat(sC, 12 + o, ci, cj, m, nn, batch, false))) return r;
   if ((r = check_mat(sD, 15 + o, di, dj, m, nn, batch, true))) return r;
   if (m == 0 || nn == 0 || batch == 0) return 0;  // level3.py:91-92, 130-131
@@ -119,19 +121,85 @@ static int gemm_common(bool syrk, int m, int n, int k, double alpha, const pb_dm
   g.tmaC = tma_ok(sC);
   g.skip = skip;
   cudaStream_t st = (cudaStream_t)stream;
-  return finish(syrk ? run_syrk_ln(g, st) : run_gemm_nt(g, st));
+  return finish(syrk ? run_syrk_ln(g, st) : nn_b ? run_gemm_nn(g, st) : run_gemm_nt(g, st));
 }
 
 int pb_dgemm_nt(int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
                 int bi, int bj, double beta, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
                 int dj, void *stream) {
-  return gemm_common(false, m, n, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+  return gemm_common(0, m, n, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+}
+
+int pb_dgemm_nn(int m, int n, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
+                int bi, int bj, double beta, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
+                int dj, void *stream) {
+  return gemm_common(2, m, n, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+}
+
+int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                  int bj, const pb_dmat_batch *sD, int di, int dj, void *stream) {
+  // positions: m1 n2 alpha3 A4 ai5 aj6 B7 bi8 bj9 D10 di11 dj12 (level3.py:140-153)
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sD) return fail_arg(10, "null matrix descriptor");
+  const int batch = sD->batch;
+  int r;
+  if ((r = check_mat(sA, 4, ai, aj, n, n, batch, false))) return r;
+  if ((r = check_mat(sB, 7, bi, bj, m, n, batch, false))) return r;
+  if ((r = check_mat(sD, 10, di, dj, m, n, batch, true))) return r;
+  if (m == 0 || n == 0 || batch == 0) return 0;  // level3.py:148-149
+  // D = alpha * X * T as an NN product: the streamed operand X (= B) is the
+  // kernel's A, the triangular factor T (= A) its B
+  cudaStream_t st = (cudaStream_t)stream;
+  // In place (D on B's storage, test_level3.py:190-195): tiles of D would
+  // overwrite columns of B other column tiles still read once n spans
+  // several tiles, so B's window is first copied to a stream-ordered
+  // workspace (one warp-tile spans all n <= 24 columns: no copy needed).
+  pb_dmat_batch w;
+  double *wp = nullptr;
+  const pb_dmat_batch *sX = sB;
+  int xi = bi, xj = bj;
+  if (sD->pA == sB->pA && n > 24) {
+    memset(&w, 0, sizeof w);
+    w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
+    w.stride = (int64_t)((m + 3) & ~3) * w.cn;
+    if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
+    w.pA = wp;
+    CopyArgs c;
+    memset(&c, 0, sizeof c);
+    c.m = m, c.n = n;
+    c.S = to_mat(sB), c.D = to_mat(&w);
+    c.si = bi, c.sj = bj;
+    c.batch = batch;
+    if ((r = finish(run_gecp(c, st)))) {
+      cudaFreeAsync(wp, st);
+      return r;
+    }
+    sX = &w, xi = 0, xj = 0;
+  }
+  GemmArgs g;
+  g.m = m, g.n = n, g.k = n;
+  g.alpha = alpha, g.beta = 0.0;
+  g.A = to_mat(sX), g.B = to_mat(sA), g.C = to_mat(sD), g.D = to_mat(sD);
+  g.ai = xi, g.aj = xj, g.bi = ai, g.bj = aj, g.ci = di, g.cj = dj, g.di = di, g.dj = dj;
+  g.batch = batch;
+  g.vecA = vec16_ok(sX, xi);
+  g.vecB = vec16_ok(sA, ai);
+  g.tma = tma_ok(sA) && tma_ok(sX);
+  g.tmaC = false;
+  g.skip = nullptr;
+  r = finish(run_trmm_rlnn(g, st));
+  if (wp) {
+    const int rf = finish(cudaFreeAsync(wp, st));
+    if (!r) r = rf;
+  }
+  return r;
 }
 
 int pb_dsyrk_ln(int m, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
                 int bj, double beta, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
                 void *stream) {
-  return gemm_common(true, m, 0, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
+  return gemm_common(1, m, 0, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
 }
 
 // ---- trsm_rltn ----------------------------------------------------------
@@ -247,6 +315,58 @@ int pb_dpotrf_l(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_
   if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
   if (!info) return fail_arg(9, "info is required");
   return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, (cudaStream_t)stream);
+}
+
+int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                      int bj, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+                      int32_t *info, void *stream) {
+  // positions: m1 n2 k3 A4 ai5 aj6 B7 bi8 bj9 C10 ci11 cj12 D13 di14 dj15 info16 (level3.py:353-391)
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0 || n > m) return fail_arg(2, "syrk_potrf_ln needs 0 <= n <= m");
+  if (k < 0) return fail_arg(3, "negative size");
+  if (!sD) return fail_arg(13, "null matrix descriptor");
+  const int batch = sD->batch;
+  int r;
+  if ((r = check_mat(sA, 4, ai, aj, m, k, batch, false))) return r;
+  if ((r = check_mat(sB, 7, bi, bj, n, k, batch, false))) return r;
+  if ((r = check_mat(sC, 10, ci, cj, m, n, batch, false))) return r;
+  if ((r = check_mat(sD, 13, di, dj, m, n, batch, true))) return r;
+  if (n == 0 || batch == 0) return 0;  // level3.py:370-371
+  if (!sD->dA) return fail_arg(13, "output needs diag_inv storage");
+  if (!info) return fail_arg(16, "info is required");
+  cudaStream_t st = (cudaStream_t)stream;
+  // W = lower trapezoid of C + A*B^T in a stream-ordered workspace, then
+  // potrf_l(W -> D).  syrk_potrf_drv (ccore.pyx:908-941) walks the same
+  // block rows as potrf_drv with the tile input C + A*B^T, so D's contents
+  // on a failed pivot follow potrf_l's rule on W.
+  pb_dmat_batch w;
+  memset(&w, 0, sizeof w);
+  w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
+  w.stride = (int64_t)((m + 3) & ~3) * w.cn;
+  double *wp = nullptr;
+  if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
+  w.pA = wp;
+  GemmArgs g;
+  g.n = n, g.k = k, g.alpha = 1.0, g.beta = 1.0;
+  g.A = to_mat(sA), g.B = to_mat(sB), g.C = to_mat(sC), g.D = to_mat(&w);
+  g.batch = batch;
+  g.tma = tma_ok(sA) && tma_ok(sB);
+  g.tmaC = tma_ok(sC);
+  g.skip = nullptr;
+  // top n x n block: lower triangle only
+  g.m = n;
+  g.ai = ai, g.aj = aj, g.bi = bi, g.bj = bj, g.ci = ci, g.cj = cj, g.di = 0, g.dj = 0;
+  g.vecA = vec16_ok(sA, ai), g.vecB = vec16_ok(sB, bi);
+  r = finish(run_syrk_ln(g, st));
+  if (!r && m > n) {  // trailing (m - n) x n rows: full product
+    g.m = m - n;
+    g.ai = ai + n, g.ci = ci + n, g.di = n;
+    g.vecA = vec16_ok(sA, ai + n);
+    r = finish(run_gemm_nt(g, st));
+  }
+  if (!r) r = potrf_run(m, n, &w, 0, 0, sD, di, dj, info, 0, 0, st);
+  const int rf = finish(cudaFreeAsync(wp, st));
+  return r ? r : rf;
 }
 
 // ---- pack / unpack / gecp ------------------------------------------------

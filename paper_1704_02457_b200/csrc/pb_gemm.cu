@@ -57,17 +57,51 @@ __device__ __forceinline__ double epilogue_value(const GemmArgs &g, ix r, ix c, 
   return store_rule(g.alpha, acc, g.beta, cv);
 }
 
-// ---------------------------------------------------------------------------
-// gemm_direct: warp per item, fragments straight from global memory.
+__device__ __forceinline__ void unit_coords(ix u, ix tiles_m, ix tiles_n, bool syrk, ix &b, ix &tm, ix &tn) {
+  if (!syrk) {
+    const ix per = tiles_m * tiles_n;
+    b = u / per;
+    const ix t = u % per;
+    tm = t / tiles_n;
+    tn = t % tiles_n;
+  } else {
+    const ix per = tiles_m * (tiles_m + 1) / 2;
+    b = u / per;
+    ix t = u % per;
+    // lower-triangular tile index -> (tm, tn), tn <= tm
+    ix r = (ix)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (r * (r + 1) / 2 > t) --r;
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    tm = r;
+    tn = t - r * (r + 1) / 2;
+  }
+}
 
-template <int MT, int NT, bool SYRK>
-__global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g) {
+// B-operand modes.  BOP_NT: B is n x k, fragments read along B's rows
+// (gemm_nt / syrk).  BOP_NN: B is k x n read down its columns across
+// panels (gemm_nn_drv ccore.pyx:774-801).  BOP_TRI: BOP_NN with B an n x n
+// lower-triangular right factor, entries above its diagonal read as 0 and
+// D = alpha*acc with no C term (trmm_rlnn_drv ccore.pyx:834-852,
+// _ktrmm_core :305-349).
+enum { BOP_NT = 0, BOP_NN = 1, BOP_TRI = 2 };
+
+// ---------------------------------------------------------------------------
+// gemm_direct: one warp per (item, 8MT x 8NT output tile), fragments
+// straight from global memory.  Used for tiny items (one tile per item)
+// and as the any-alignment fallback of the NN modes.
+
+template <int MT, int NT, bool SYRK, int BOP = BOP_NT>
+__global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
   const int lane = threadIdx.x & 31;
   const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const ix nwarps = (ix)gridDim.x * (blockDim.x >> 5);
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / k-col
-  for (ix b = warp; b < g.batch; b += nwarps) {
+  const ix ncols = SYRK ? g.m : g.n;
+  for (ix u = warp; u < nunits; u += nwarps) {
+    ix b, tm, tn;
+    unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
     if (g.skip && g.skip[b] >= 0) continue;
+    const ix rbase = tm * (8 * MT), cbase = tn * (8 * NT);
     const double *A = g.A.item(b);
     const double *B = g.B.item(b);
     const double *C = g.C.item(b);
@@ -82,22 +116,29 @@ __global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g) {
         for (int e = 0; e < 2; ++e) {
           acc[i][j][e] = 0.0;
           cv[i][j][e] = 0.0;
-          const ix r = 8 * i + fr, c = 8 * j + 2 * fc + e;
-          if (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n)) cv[i][j][e] = C[eo(g.ci + r, g.cj + c, g.C.cn)];
+          const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
+          if (BOP != BOP_TRI && g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n))
+            cv[i][j][e] = C[eo(g.ci + r, g.cj + c, g.C.cn)];
         }
-    if (g.alpha != 0.0) {
-      for (int k0 = 0; k0 < g.k; k0 += 4) {
-        const int l = k0 + fc;
+    if (g.alpha != 0.0 || BOP == BOP_TRI) {
+      // triangular B: rows above this tile's first column are all zero
+      const ix kstart = BOP == BOP_TRI ? (cbase & ~(ix)3) : 0;
+      for (ix k0 = kstart; k0 < g.k; k0 += 4) {
+        const ix l = k0 + fc;
         double a[MT], bb[NT];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-          const ix r = 8 * i + fr;
+          const ix r = rbase + 8 * i + fr;
           a[i] = (r < g.m && l < g.k) ? ldg_nc(A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const ix r = 8 * j + fr;
-          bb[j] = (r < g.n && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
+          const ix r = cbase + 8 * j + fr;
+          if (BOP == BOP_NT)
+            bb[j] = (r < ncols && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
+          else
+            bb[j] = (r < ncols && l < g.k && (BOP != BOP_TRI || l >= r)) ? ldg_nc(B + eo(g.bi + l, g.bj + r, g.B.cn))
+                                                                         : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < MT; ++i)
@@ -112,9 +153,10 @@ __global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g) {
       for (int j = 0; j < NT; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const ix r = 8 * i + fr, c = 8 * j + 2 * fc + e;
+          const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
           if (in_store<SYRK>(r, c, g.m, g.n))
-            D[eo(g.di + r, g.dj + c, g.D.cn)] = epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
+            D[eo(g.di + r, g.dj + c, g.D.cn)] = BOP == BOP_TRI ? __dmul_rn(g.alpha, acc[i][j][e])
+                                                               : epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
         }
   }
 }
@@ -161,26 +203,6 @@ __device__ __forceinline__ void load_panel_tile(double *s, const double *G, ix c
       const double *src = ok ? G + eo(gi + R, gj + L, cn) : G;
       cp_async8(s + p * 4 * KC + 4 * l + rr, src, ok ? 8 : 0);
     }
-  }
-}
-
-__device__ __forceinline__ void unit_coords(ix u, ix tiles_m, ix tiles_n, bool syrk, ix &b, ix &tm, ix &tn) {
-  if (!syrk) {
-    const ix per = tiles_m * tiles_n;
-    b = u / per;
-    const ix t = u % per;
-    tm = t / tiles_n;
-    tn = t % tiles_n;
-  } else {
-    const ix per = tiles_m * (tiles_m + 1) / 2;
-    b = u / per;
-    ix t = u % per;
-    // lower-triangular tile index -> (tm, tn), tn <= tm
-    ix r = (ix)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while (r * (r + 1) / 2 > t) --r;
-    while ((r + 1) * (r + 2) / 2 <= t) ++r;
-    tm = r;
-    tn = t - r * (r + 1) / 2;
   }
 }
 
@@ -298,30 +320,42 @@ __global__ void __launch_bounds__(TiledCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS
 // extra panel and index fragments with the constant row shift ai % 4, so
 // unaligned stream operands need no repack (level3.py:56-62).
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, int CB>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, int CB, int BOP = BOP_NT>
 struct TmaCfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NWARPS = WARPS_M * WARPS_N;      // consumer (MMA) warps
   static constexpr int NTHREADS = 32 * (NWARPS + 1);    // + one producer (TMA) warp
   static constexpr int MT = WM / 8, NT = WN / 8;
-  static constexpr int PA = BM / 4 + 1, PB = BN / 4 + 1;  // panels per operand tile
-  static constexpr int A_ELEMS = PA * 4 * KC, B_ELEMS = PB * 4 * KC;
+  static constexpr int PA = BM / 4 + 1;                  // panels per A tile
+  // B tile: NT -> BN/4+1 panels x KC columns; NN -> KC/4+1 panels x BN columns
+  static constexpr int B_PANEL = BOP == BOP_NT ? KC : BN;
+  static constexpr int PB = BOP == BOP_NT ? BN / 4 + 1 : KC / 4 + 1;
+  static constexpr int A_ELEMS = PA * 4 * KC, B_ELEMS = PB * 4 * B_PANEL;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr int C_ELEMS = PA * 4 * BN;            // one C tile (panels x BN columns)
   static constexpr size_t SMEM = sizeof(double) * (STAGE_ELEMS * STAGES + C_ELEMS * CB) + 16 * (STAGES + CB);
 };
+
+// First k-chunk a unit needs: a lower-triangular B has no nonzero rows
+// above the tile's first column.
+template <int BN, int KC, int BOP>
+__device__ __forceinline__ ix first_chunk(ix tn) {
+  return BOP == BOP_TRI ? (tn * BN) / KC : 0;
+}
 
 // Warp-specialised: warp NWARPS is the producer (bulk copies gated by
 // per-stage "empty" mbarriers), warps 0..NWARPS-1 consume stages gated by
 // "full" mbarriers -- no CTA-wide barrier in the main loop.  With CB > 0
 // the producer also streams each unit's C tile into one of CB shared
 // buffers, so the epilogue reads C from shared memory instead of waiting
-// on global loads.
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB>
-__global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREADS, (CB >= 2 ? 1 : 2))
+// on global loads.  Both sides walk the same (unit, k-chunk) sequence; the
+// running stage counter s selects the ring slot and its phase.
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB, int BOP>
+__global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::NTHREADS, (CB >= 2 ? 1 : 2))
     gemm_tma_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
-  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>;
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
+  constexpr int BSTEP = BOP == BOP_NT ? 16 : 4 * BN;  // B fragment advance per k-step of 4
   extern __shared__ __align__(128) double smem[];
   double *cbuf = smem + Cfg::STAGE_ELEMS * STAGES;
   uint64_t *full = reinterpret_cast<uint64_t *>(cbuf + Cfg::C_ELEMS * CB);
@@ -330,12 +364,11 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
   uint64_t *cempty = cfull + CB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const ix ncols = SYRK ? g.m : g.n;
-  const bool cin = CB > 0 && g.beta != 0.0 && g.tmaC;  // C through shared memory
+  const bool cin = CB > 0 && BOP != BOP_TRI && g.beta != 0.0 && g.tmaC;  // C through shared memory
+  const bool domma = g.alpha != 0.0 || BOP == BOP_TRI;
 
-  const ix nk = g.alpha != 0.0 ? (g.k + KC - 1) / KC : 0;
-  const ix steps_per_unit = nk > 0 ? nk : 1;
+  const ix nk = domma ? (g.k + KC - 1) / KC : 0;
   const ix my_units = blockIdx.x < nunits ? (nunits - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const ix nsteps = my_units * steps_per_unit;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -355,12 +388,12 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
   if (warp == Cfg::NWARPS) {
     // ===== producer =====
     if (nk == 0 && !cin) return;
-    for (ix s = 0; s < nsteps; ++s) {
-      const ix ul = s / steps_per_unit, ch = s % steps_per_unit;
+    ix s = 0;
+    for (ix ul = 0; ul < my_units; ++ul) {
       const ix u = blockIdx.x + ul * gridDim.x;
       ix b, tm, tn;
       unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
-      if (CB > 0 && cin && ch == 0) {
+      if (CB > 0 && cin) {
         const int cb = (int)(ul % (CB > 0 ? CB : 1));
         if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / (CB > 0 ? CB : 1)) - 1) & 1));
         const ix rc = g.ci + tm * BM;
@@ -373,25 +406,42 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
         for (int p = lane; p < npc; p += 32)
           tma_load_1d(cbuf + cb * Cfg::C_ELEMS + p * 4 * BN, C + (ix)p * 4 * g.C.cn, bytes, &cfull[cb]);
       }
-      if (nk == 0) continue;
-      const int st = (int)(s % STAGES);
-      if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
-      double *sa = smem + st * Cfg::STAGE_ELEMS;
-      double *sb = sa + Cfg::A_ELEMS;
-      const ix l0 = ch * KC;
-      const int kc = (int)min((ix)KC, g.k - l0);
-      const ix ra = g.ai + tm * BM, rb = g.bi + tn * BN;
-      const ix rowsa = min((ix)BM, g.m - tm * BM), rowsb = min((ix)BN, ncols - tn * BN);
-      const int npa = (int)(((ra + rowsa - 1) >> 2) - (ra >> 2) + 1);
-      const int npb = (int)(((rb + rowsb - 1) >> 2) - (rb >> 2) + 1);
-      const unsigned bytes = 32u * kc;
-      if (lane == 0) mbar_arrive_expect_tx(&full[st], bytes * (npa + npb));
-      __syncwarp();
-      const double *A = g.A.item(b) + (ra >> 2) * 4 * g.A.cn + 4 * (g.aj + l0);
-      const double *B = g.B.item(b) + (rb >> 2) * 4 * g.B.cn + 4 * (g.bj + l0);
-      for (int p = lane; p < npa + npb; p += 32) {
-        if (p < npa) tma_load_1d(sa + p * 4 * KC, A + (ix)p * 4 * g.A.cn, bytes, &full[st]);
-        else tma_load_1d(sb + (p - npa) * 4 * KC, B + (ix)(p - npa) * 4 * g.B.cn, bytes, &full[st]);
+      for (ix ch = first_chunk<BN, KC, BOP>(tn); ch < nk; ++ch, ++s) {
+        const int st = (int)(s % STAGES);
+        if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
+        double *sa = smem + st * Cfg::STAGE_ELEMS;
+        double *sb = sa + Cfg::A_ELEMS;
+        const ix l0 = ch * KC;
+        const int kc = (int)min((ix)KC, g.k - l0);
+        const ix ra = g.ai + tm * BM;
+        const ix rowsa = min((ix)BM, g.m - tm * BM);
+        const int npa = (int)(((ra + rowsa - 1) >> 2) - (ra >> 2) + 1);
+        const unsigned bytesa = 32u * kc;
+        const double *A = g.A.item(b) + (ra >> 2) * 4 * g.A.cn + 4 * (g.aj + l0);
+        if (BOP == BOP_NT) {
+          const ix rb = g.bi + tn * BN;
+          const ix rowsb = min((ix)BN, ncols - tn * BN);
+          const int npb = (int)(((rb + rowsb - 1) >> 2) - (rb >> 2) + 1);
+          if (lane == 0) mbar_arrive_expect_tx(&full[st], bytesa * (npa + npb));
+          __syncwarp();
+          const double *B = g.B.item(b) + (rb >> 2) * 4 * g.B.cn + 4 * (g.bj + l0);
+          for (int p = lane; p < npa + npb; p += 32) {
+            if (p < npa) tma_load_1d(sa + p * 4 * KC, A + (ix)p * 4 * g.A.cn, bytesa, &full[st]);
+            else tma_load_1d(sb + (p - npa) * 4 * KC, B + (ix)(p - npa) * 4 * g.B.cn, bytesa, &full[st]);
+          }
+        } else {
+          // B rows [bi + l0, bi + l0 + kc) x columns [tn*BN, +cols): one run per panel
+          const ix rb = g.bi + l0;
+          const int npb = (int)(((rb + kc - 1) >> 2) - (rb >> 2) + 1);
+          const unsigned bytesb = 32u * (unsigned)min((ix)BN, ncols - tn * BN);
+          if (lane == 0) mbar_arrive_expect_tx(&full[st], bytesa * npa + bytesb * npb);
+          __syncwarp();
+          const double *B = g.B.item(b) + (rb >> 2) * 4 * g.B.cn + 4 * (g.bj + tn * BN);
+          for (int p = lane; p < npa + npb; p += 32) {
+            if (p < npa) tma_load_1d(sa + p * 4 * KC, A + (ix)p * 4 * g.A.cn, bytesa, &full[st]);
+            else tma_load_1d(sb + (p - npa) * 4 * BN, B + (ix)(p - npa) * 4 * g.B.cn, bytesb, &full[st]);
+          }
+        }
       }
     }
     return;
@@ -411,8 +461,13 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
   }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    const int r = airb + wn * WN + 8 * j + fr;
-    offb[j] = (r >> 2) * 4 * KC + (r & 3) + 4 * fc;
+    if (BOP == BOP_NT) {
+      const int r = airb + wn * WN + 8 * j + fr;
+      offb[j] = (r >> 2) * 4 * KC + (r & 3) + 4 * fc;
+    } else {
+      const int r = airb + fc;  // k row within the chunk
+      offb[j] = (r >> 2) * 4 * BN + (r & 3) + 4 * (wn * WN + 8 * j + fr);
+    }
   }
 
   double acc[MT][NT][2];
@@ -421,30 +476,29 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  ix b = 0, tm = 0, tn = 0;
-  for (ix s = 0; s < nsteps; ++s) {
-    const ix ul = s / steps_per_unit, ch = s % steps_per_unit;
-    if (ch == 0) {
-      const ix u = blockIdx.x + ul * gridDim.x;
-      unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
-    }
+  ix s = 0;
+  for (ix ul = 0; ul < my_units; ++ul) {
+    ix b, tm, tn;
+    unit_coords(blockIdx.x + ul * gridDim.x, tiles_m, tiles_n, SYRK, b, tm, tn);
     const ix rbase = tm * BM + wm * WM, cbase = tn * BN + wn * WN;
-    if (nk > 0) {
+    const bool active = !SYRK || (cbase <= rbase + WM - 1);
+    for (ix ch = first_chunk<BN, KC, BOP>(tn); ch < nk; ++ch, ++s) {
       const int st = (int)(s % STAGES);
       mbar_wait(&full[st], (unsigned)((s / STAGES) & 1));
       const double *sa = smem + st * Cfg::STAGE_ELEMS;
       const double *sb = sa + Cfg::A_ELEMS;
-      const bool active = !SYRK || (cbase <= rbase + WM - 1);
       const int kc = (int)min((ix)KC, g.k - ch * KC);
+      // triangular B: this chunk crosses the diagonal of the warp's columns
+      const bool tri = BOP == BOP_TRI && ch * KC < cbase + WN;
       if (active) {
-        if (kc == KC) {
+        if (kc == KC && !tri) {
 #pragma unroll
           for (int kk = 0; kk < KC / 4; ++kk) {
             double a[MT], bb[NT];
 #pragma unroll
             for (int i = 0; i < MT; ++i) a[i] = sa[offa[i] + 16 * kk];
 #pragma unroll
-            for (int j = 0; j < NT; ++j) bb[j] = sb[offb[j] + 16 * kk];
+            for (int j = 0; j < NT; ++j) bb[j] = sb[offb[j] + BSTEP * kk];
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -452,12 +506,16 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
           }
         } else {
           for (int kk = 0; 4 * kk < kc; ++kk) {
-            const bool okc = 4 * kk + fc < kc;
+            const int lk = 4 * kk + fc;
+            const bool okc = lk < kc;
             double a[MT], bb[NT];
 #pragma unroll
             for (int i = 0; i < MT; ++i) a[i] = okc ? sa[offa[i] + 16 * kk] : 0.0;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) bb[j] = okc ? sb[offb[j] + 16 * kk] : 0.0;
+            for (int j = 0; j < NT; ++j) {
+              const bool okt = BOP != BOP_TRI || ch * KC + lk >= cbase + 8 * j + fr;
+              bb[j] = (okc && okt) ? sb[offb[j] + BSTEP * kk] : 0.0;
+            }
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -468,7 +526,7 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    if (ch == steps_per_unit - 1) {
+    {
       double *D = g.D.item(b);
       const double *C = g.C.item(b);
       const bool skip = g.skip && g.skip[b] >= 0;
@@ -493,7 +551,7 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
-              cv[i][j][e] = (g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n))
+              cv[i][j][e] = (BOP != BOP_TRI && g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n))
                                 ? ldg_nc(C + eo(g.ci + r, g.cj + c, g.C.cn))
                                 : 0.0;
             }
@@ -506,7 +564,9 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>::NTHREA
           for (int e = 0; e < 2; ++e) {
             const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
             if (!skip && in_store<SYRK>(r, c, g.m, g.n))
-              D[eo(g.di + r, g.dj + c, g.D.cn)] = epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
+              D[eo(g.di + r, g.dj + c, g.D.cn)] = BOP == BOP_TRI
+                                                      ? __dmul_rn(g.alpha, acc[i][j][e])
+                                                      : epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
             acc[i][j][e] = 0.0;
           }
     }
@@ -658,24 +718,27 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int MT, int NT, bool SYRK>
+template <int MT, int NT, bool SYRK, int BOP = BOP_NT>
 static cudaError_t launch_direct(const GemmArgs &g, cudaStream_t st) {
   const int threads = 256;
-  const ix warps_needed = g.batch;
-  ix blocks = (warps_needed + 7) / 8;
+  const ix tiles_m = (g.m + 8 * MT - 1) / (8 * MT);
+  const ix tiles_n = SYRK ? tiles_m : (g.n + 8 * NT - 1) / (8 * NT);
+  const ix per = SYRK ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  const ix nunits = per * g.batch;
+  ix blocks = (nunits + 7) / 8;
   const ix cap = (ix)num_sms() * 8 * 8;  // ~8 resident CTAs of 8 warps per SM, a few waves
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  gemm_direct_kernel<MT, NT, SYRK><<<(unsigned)blocks, threads, 0, st>>>(g);
+  gemm_direct_kernel<MT, NT, SYRK, BOP><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
   note_launch();
   return cudaGetLastError();
 }
 
-template <bool SYRK>
+template <bool SYRK, int BOP = BOP_NT>
 static cudaError_t dispatch_direct(const GemmArgs &g, cudaStream_t st) {
   const int mt = (int)((g.m + 7) / 8), nt = (int)(((SYRK ? g.m : g.n) + 7) / 8);
 #define PB_DIRECT(M_, N_) \
-  if (mt == M_ && nt == N_) return launch_direct<M_, N_, SYRK>(g, st);
+  if (mt == M_ && nt == N_) return launch_direct<M_, N_, SYRK, BOP>(g, st);
   PB_DIRECT(1, 1) PB_DIRECT(1, 2) PB_DIRECT(1, 3) PB_DIRECT(2, 1) PB_DIRECT(2, 2) PB_DIRECT(2, 3)
   PB_DIRECT(3, 1) PB_DIRECT(3, 2) PB_DIRECT(3, 3)
 #undef PB_DIRECT
@@ -706,10 +769,10 @@ static cudaError_t launch_tiled(const GemmArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB = 0>
+template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB = 0, int BOP = BOP_NT>
 static cudaError_t launch_tma(const GemmArgs &g, cudaStream_t st) {
-  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB>;
-  auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK, CB>;
+  using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>;
+  auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK, CB, BOP>;
   static bool configured = false;
   static int occ = 1;
   if (!configured) {
@@ -768,7 +831,32 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   return launch_tiled<64, 64, 32, 32, 32, 2, SYRK>(g, st);
 }
 
+// gemm_nn / trmm_rlnn: B read down its columns (BOP_NN / BOP_TRI).
+template <int BOP>
+static cudaError_t dispatch_nn(const GemmArgs &g, cudaStream_t st) {
+  const ix big = g.m > g.n ? g.m : g.n;
+  if (big <= 24) return dispatch_direct<false, BOP>(g, st);
+  if (!g.tma) return launch_direct<3, 3, false, BOP>(g, st);  // any alignment
+  int T = 64;
+  double best = 1e30;
+  for (int t : {64, 48, 32}) {
+    const double area = (double)((g.m + t - 1) / t * t) * (double)((g.n + t - 1) / t * t);
+    if (area < best * 0.999) best = area, T = t;
+  }
+  const bool cs = BOP == BOP_NN && g.beta != 0.0 && g.tmaC;
+#define PB_TMA_NN(T_, WM_)                                                                     \
+  if (T == T_) {                                                                               \
+    if (cs) return launch_tma<T_, T_, WM_, 16, 32, 2, false, (BOP == BOP_NN ? 1 : 0), BOP>(g, st); \
+    return launch_tma<T_, T_, WM_, 16, 32, 3, false, 0, BOP>(g, st);                             \
+  }
+  PB_TMA_NN(64, 32) PB_TMA_NN(48, 24) PB_TMA_NN(32, 16)
+#undef PB_TMA_NN
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t run_gemm_nt(const GemmArgs &g, cudaStream_t st) { return dispatch_gemm<false>(g, st); }
+cudaError_t run_gemm_nn(const GemmArgs &g, cudaStream_t st) { return dispatch_nn<BOP_NN>(g, st); }
+cudaError_t run_trmm_rlnn(const GemmArgs &g, cudaStream_t st) { return dispatch_nn<BOP_TRI>(g, st); }
 cudaError_t run_syrk_ln(const GemmArgs &g, cudaStream_t st) { return dispatch_gemm<true>(g, st); }
 
 }  // namespace pb

@@ -56,6 +56,8 @@ int num_sms();
 
 cudaError_t run_gemm_nt(const GemmArgs &g, cudaStream_t st);
 cudaError_t run_syrk_ln(const GemmArgs &g, cudaStream_t st);
+cudaError_t run_gemm_nn(const GemmArgs &g, cudaStream_t st);
+cudaError_t run_trmm_rlnn(const GemmArgs &g, cudaStream_t st);
 cudaError_t run_trsm_rltn(const TrsmArgs &g, cudaStream_t st);
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_pack(const CopyArgs &g, cudaStream_t st);

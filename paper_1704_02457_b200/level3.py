@@ -106,6 +106,43 @@ def gemm_nt(m, n, k, alpha, A, B, beta, C, D):
                  float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
 
 
+def gemm_nn(m, n, k, alpha, A, B, beta, C, D):
+    """D = alpha*A*B + beta*C with A m x k and B k x n, for every item
+    (level3.py:101-117).  Unaligned A windows are read in place instead of
+    the reference's repack (level3.py:113)."""
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, m, k, "A")
+    _check(b, bi, bj, k, n, "B")
+    _check(c, ci, cj, m, n, "C")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, a, b, c)
+    if m == 0 or n == 0 or nb == 0:
+        return
+    da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
+    _native.call("pb_dgemm_nn", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+
+
+def trmm_rlnn(m, n, alpha, A, B, D):
+    """D = alpha*B*A with A an n x n lower-triangular right factor
+    (level3.py:140-153); A's strict upper triangle is never read."""
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, n, n, "A")
+    _check(b, bi, bj, m, n, "B")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, a, b)
+    if m == 0 or n == 0 or nb == 0:
+        return
+    da, db, dd = (x.descriptor(nb) for x in (a, b, d))
+    _native.call("pb_dtrmm_rlnn", m, n, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                 ctypes.byref(dd), di, dj, _stream(d.device))
+
+
 def syrk_ln(m, k, alpha, A, B, beta, C, D):
     """Lower triangle of D = alpha*A*B' + beta*C (m x m); upper untouched."""
     a, ai, aj = _ref(A, "A")
@@ -205,6 +242,45 @@ def potrf_l(m, C, D, n=None, check=True):
             _mark_diag(d, dj, 0, False)
             raise NotPositiveDefiniteError(
                 f"potrf_l: non-positive pivot at index {f[1]} (batch item {f[0]})", f[1],
+                batch_index=f[0], info=info)
+    _mark_diag(d, dj, n, di == dj)
+    return info
+
+
+def syrk_potrf_ln(m, k, A, B, C, D, n=None, check=True):
+    """D = chol(lower(C + A*B')) for every item (level3.py:353-391).
+
+    A is m x k, B n x k, C and D m x n with n <= m.  Matches syrk_ln
+    (alpha = beta = 1) followed by potrf_l up to rounding, as the
+    reference's docstring states; info / diag_inv / failure rules are
+    potrf_l's.
+    """
+    if n is None:
+        n = m
+    if n > m:
+        raise DimensionError(f"syrk_potrf_ln needs n <= m, got m={m} n={n}")
+    a, ai, aj = _ref(A, "A")
+    b, bi, bj = _ref(B, "B")
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(a, ai, aj, m, k, "A")
+    _check(b, bi, bj, n, k, "B")
+    _check(c, ci, cj, m, n, "C")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, a, b, c)
+    if n == 0 or nb == 0:
+        return None
+    info = torch.empty(nb, dtype=torch.int32, device=d.device)
+    da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
+    _native.call("pb_dsyrk_potrf_ln", m, n, k, ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                 ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr()),
+                 _stream(d.device))
+    if check:
+        f = _first_failure(info)
+        if f is not None:
+            _mark_diag(d, dj, 0, False)
+            raise NotPositiveDefiniteError(
+                f"syrk_potrf_ln: non-positive pivot at index {f[1]} (batch item {f[0]})", f[1],
                 batch_index=f[0], info=info)
     _mark_diag(d, dj, n, di == dj)
     return info

@@ -185,6 +185,105 @@ def potrf_case(name, rng, m, c, n=None, oc=(0, 0), od=(0, 0), in_place=False, df
     record(name, "potrf_l", p, {"C": C, "D": D}, lambda: level3.potrf_l(m, C.ref(*oc), D.ref(*od), n=n))
 
 
+def gemm_nn_case(name, rng, m, n, k, alpha, beta, oa=(0, 0), ob=(0, 0), oc=(0, 0), od=(0, 0),
+                 a=None, b=None, c=None, alias_dc=False, dfill=0.0):
+    a = rng.uniform(-1, 1, (m, k)) if a is None else a
+    b = rng.uniform(-1, 1, (k, n)) if b is None else b
+    c = rng.uniform(-1, 1, (m, n)) if c is None else c
+    A = zmat(oa[0] + m + 3, oa[1] + k + 2)
+    B = zmat(ob[0] + k + 1, ob[1] + n + 3)
+    C = zmat(oc[0] + m + 2, oc[1] + n + 1)
+    put(A, *oa, a)
+    put(B, *ob, b)
+    put(C, *oc, c)
+    if alias_dc:
+        D, od = C, oc
+    else:
+        D = zmat(od[0] + m + 1, od[1] + n + 2, fill=dfill)
+    p = dict(m=m, n=n, k=k, alpha=alpha, beta=beta, ai=oa[0], aj=oa[1], bi=ob[0], bj=ob[1], ci=oc[0], cj=oc[1],
+             di=od[0], dj=od[1])
+    record(name, "gemm_nn", p, {"A": A, "B": B, "C": C, "D": D},
+           lambda: level3.gemm_nn(m, n, k, alpha, A.ref(*oa), B.ref(*ob), beta, C.ref(*oc), D.ref(*od)))
+
+
+def trmm_case(name, rng, m, n, alpha, oa=(0, 0), ob=(0, 0), od=(0, 0), t=None, b=None, in_place=False,
+              poison=True, dfill=0.0):
+    t = np.tril(rng.uniform(-1, 1, (n, n))) if t is None else t
+    if poison:
+        t = t + np.triu(np.full((n, n), np.nan), 1)
+    b = rng.uniform(-1, 1, (m, n)) if b is None else b
+    A = zmat(oa[0] + n + 1, oa[1] + n + 2)
+    put(A, *oa, t)
+    B = zmat(ob[0] + m + 2, ob[1] + n + 1)
+    put(B, *ob, b)
+    if in_place:
+        D, od = B, ob
+    else:
+        D = zmat(od[0] + m + 1, od[1] + n + 1, fill=dfill)
+    p = dict(m=m, n=n, alpha=alpha, ai=oa[0], aj=oa[1], bi=ob[0], bj=ob[1], di=od[0], dj=od[1])
+    record(name, "trmm_rlnn", p, {"A": A, "B": B, "D": D},
+           lambda: level3.trmm_rlnn(m, n, alpha, A.ref(*oa), B.ref(*ob), D.ref(*od)))
+
+
+def syrk_potrf_case(name, rng, m, k, n=None, oa=(0, 0), ob=(0, 0), oc=(0, 0), od=(0, 0), a=None, b=None, c=None,
+                    same_ab=True, dfill=0.0):
+    n = m if n is None else n
+    a = rng.uniform(-1, 1, (m, k)) if a is None else a
+    if c is None:
+        c = rng.uniform(-1, 1, (m, n))
+        c[:n, :n] = spd(rng, n)
+    A = zmat(oa[0] + m + 2, oa[1] + k + 1)
+    put(A, *oa, a)
+    if same_ab:
+        B, ob = A, oa
+    else:
+        b = rng.uniform(-1, 1, (n, k)) if b is None else b
+        B = zmat(ob[0] + n + 1, ob[1] + k + 2)
+        put(B, *ob, b)
+    C = zmat(oc[0] + m + 1, oc[1] + n + 1)
+    put(C, *oc, c)
+    D = zmat(od[0] + m + 2, od[1] + n + 1, fill=dfill)
+    p = dict(m=m, n=n, k=k, ai=oa[0], aj=oa[1], bi=ob[0], bj=ob[1], ci=oc[0], cj=oc[1], di=od[0], dj=od[1])
+    record(name, "syrk_potrf_ln", p, {"A": A, "B": B, "C": C, "D": D},
+           lambda: level3.syrk_potrf_ln(m, k, A.ref(*oa), B.ref(*ob), C.ref(*oc), D.ref(*od), n=n))
+
+
+RICCATI = []
+
+
+def riccati_case(name, rng, nx, nu, N, fail_stage=None):
+    """apps.riccati_factorize on random stable data; records the packed
+    stage inputs and every stage factor (apps.py:231-254)."""
+    from panelblas import apps
+    A = rng.uniform(-0.5, 0.5, (N, nx, nx)) + 0.8 * np.eye(nx)
+    B = rng.uniform(-1, 1, (N, nx, nu))
+    Q = np.stack([spd(rng, nx) for _ in range(N)])
+    R = np.stack([spd(rng, nu) if nu else np.zeros((0, 0)) for _ in range(N)])
+    S = rng.uniform(-0.1, 0.1, (N, nu, nx))
+    P = spd(rng, nx)
+    if fail_stage is not None:
+        R[fail_stage][0, 0] = -1e6
+    dims = apps.OcpDims(nx, nu, N)
+    data = apps.OcpData.from_arrays(dims, A, B, Q, R, S, P)
+    key = f"r{len(RICCATI):02d}"
+    for n_, st in enumerate(data.stages):
+        ARRAYS[f"{key}/bat{n_}"] = raw(st.bat)
+        ARRAYS[f"{key}/rsq{n_}"] = raw(st.rsq)
+    ARRAYS[f"{key}/P"] = raw(data.p_panel)
+    status, msg = -1, ""
+    ws = apps.RiccatiWorkspace(dims)  # zero the workspace: allocate_panel_matrix does not
+    for mat in [ws.cbuf, ws.terminal] + ws.factors:
+        np.frombuffer(mat._base, dtype=np.float64)[:] = 0.0
+    try:
+        fac = apps.riccati_factorize(data, ws)
+        for n_, f in enumerate(fac):
+            ARRAYS[f"{key}/F{n_}"] = raw(f.full)
+            ARRAYS[f"{key}/P{n_}"] = f.cost_to_go()
+    except FactorizationError as e:
+        status, msg = int(e.index), str(e)
+    RICCATI.append({"key": key, "name": name, "nx": nx, "nu": nu, "N": N, "status": status, "msg": msg})
+
+
 def pack_case(name, rng, m, n, od):
     arr = rng.uniform(-1, 1, (m, n))
     from panelblas.matstore import ColMatrix
@@ -261,8 +360,45 @@ def main():
     for (m, n, od) in [(2, 2, (0, 0)), (1, 1, (6, 3)), (7, 5, (3, 1)), (13, 9, (2, 5)), (0, 4, (1, 1))]:
         pack_case(f"pack_{m}x{n}", rng, m, n, od)
 
+    # ---- next tier: gemm_nn, trmm_rlnn, syrk_potrf_ln, riccati
+    gemm_nn_case("gemm_nn_kat_2x2", rng, 2, 2, 2, 1.0, 0.0, a=np.array([[1.0, 2], [3, 4]]),
+                 b=np.array([[5.0, 6], [7, 8]]))
+    for m, n, k in [(5, 3, 7), (1, 1, 1), (16, 16, 16), (13, 9, 11), (4, 20, 2), (33, 7, 5), (40, 36, 33),
+                    (64, 64, 64), (70, 17, 9), (24, 130, 40)]:
+        gemm_nn_case(f"gemm_nn_{m}x{n}x{k}", rng, m, n, k, 1.5, -0.5)
+    gemm_nn_case("gemm_nn_k0", rng, 5, 3, 0, 1.0, -2.0)
+    gemm_nn_case("gemm_nn_beta0", rng, 9, 6, 5, 1.0, 0.0, c=np.full((9, 6), np.nan))
+    gemm_nn_case("gemm_nn_alpha0_nan", rng, 8, 2, 7, 0.0, 1.0, a=np.full((8, 7), np.nan),
+                 b=np.full((7, 2), np.nan))
+    gemm_nn_case("gemm_nn_unaligned", rng, 10, 10, 6, 1.0, 1.0, oa=(3, 2), ob=(1, 3), oc=(2, 2), od=(1, 1))
+    gemm_nn_case("gemm_nn_unaligned_big", rng, 37, 45, 29, -1.0, 0.5, oa=(5, 1), ob=(2, 3), oc=(7, 2), od=(3, 1),
+                 dfill=3.5)
+    gemm_nn_case("gemm_nn_alias_dc", rng, 9, 6, 5, 1.0, 0.5, alias_dc=True)
+    trmm_case("trmm_identity", rng, 5, 4, 2.5, t=np.eye(4), poison=False)
+    trmm_case("trmm_scalar", rng, 3, 1, 1.0, t=np.array([[2.0]]), b=np.array([[1.0], [2.0], [3.0]]))
+    for m, n in [(9, 6), (4, 5), (1, 1), (8, 8), (13, 7), (24, 16), (40, 40), (72, 48), (33, 70)]:
+        trmm_case(f"trmm_{m}x{n}", rng, m, n, 1.0)
+    trmm_case("trmm_in_place", rng, 7, 6, 1.0, in_place=True)
+    trmm_case("trmm_in_place_wide", rng, 20, 40, -1.0, in_place=True)
+    trmm_case("trmm_unaligned", rng, 11, 9, 0.5, oa=(3, 2), ob=(1, 1), od=(2, 3), dfill=3.5)
+    trmm_case("trmm_alpha0", rng, 6, 5, 0.0)
+    syrk_potrf_case("syrk_potrf_k0", rng, 6, 0)
+    for m, k in [(5, 3), (12, 8), (17, 4), (8, 8), (24, 16), (40, 33)]:
+        syrk_potrf_case(f"syrk_potrf_{m}x{k}", rng, m, k)
+    syrk_potrf_case("syrk_potrf_rect", rng, 11, 4, n=6, same_ab=False)
+    syrk_potrf_case("syrk_potrf_unaligned", rng, 10, 5, oa=(1, 2), oc=(3, 1), od=(2, 2), dfill=2.5)
+    cfail = spd(rng, 9)
+    cfail[6, 6] = -1e3
+    syrk_potrf_case("syrk_potrf_fail6", rng, 9, 3, c=cfail, dfill=2.5)
+    riccati_case("riccati_2x1x3", rng, 2, 1, 3)
+    riccati_case("riccati_8x8x5", rng, 8, 8, 5)
+    riccati_case("riccati_6x3x4", rng, 6, 3, 4)
+    riccati_case("riccati_16x8x3", rng, 16, 8, 3)
+    riccati_case("riccati_fail", rng, 4, 2, 4, fail_stage=1)
+
     out = os.path.join(HERE, "golden_v1.npz")
-    ARRAYS["manifest"] = np.array(json.dumps({"backend": pb.backend_name(), "cases": CASES}))
+    ARRAYS["manifest"] = np.array(json.dumps({"backend": pb.backend_name(), "cases": CASES,
+                                              "riccati": RICCATI}))
     np.savez_compressed(out, **ARRAYS)
     print(f"wrote {len(CASES)} cases to {out} (reference backend {pb.backend_name()})")
 

@@ -39,6 +39,18 @@ def run_oracle(case, mats, z=None):
     if op == "potrf_l":
         info = O.potrf_l(p["m"], mats["C"], p["ci"], p["cj"], mats["D"], p["di"], p["dj"], n=p["n"])
         return int(info[0])
+    if op == "gemm_nn":
+        O.gemm_nn(p["m"], p["n"], p["k"], p["alpha"], mats["A"], p["ai"], p["aj"], mats["B"], p["bi"], p["bj"],
+                  p["beta"], mats["C"], p["ci"], p["cj"], mats["D"], p["di"], p["dj"])
+        return -1
+    if op == "trmm_rlnn":
+        O.trmm_rlnn(p["m"], p["n"], p["alpha"], mats["A"], p["ai"], p["aj"], mats["B"], p["bi"], p["bj"],
+                    mats["D"], p["di"], p["dj"])
+        return -1
+    if op == "syrk_potrf_ln":
+        info = O.syrk_potrf_ln(p["m"], p["k"], mats["A"], p["ai"], p["aj"], mats["B"], p["bi"], p["bj"],
+                               mats["C"], p["ci"], p["cj"], mats["D"], p["di"], p["dj"], n=p["n"])
+        return int(info[0])
     if op == "pack":
         m, n = p["m"], p["n"]
         if m * n:
@@ -63,7 +75,7 @@ def written_mask(case, lab, per, cn, status):
     def eo(i, j):
         return (i - (i & 3)) * cn + 4 * j + (i & 3)
 
-    if op in ("gemm_nt", "trsm_rltn", "pack"):
+    if op in ("gemm_nt", "gemm_nn", "trmm_rlnn", "trsm_rltn", "pack"):
         m, n = p["m"], p["n"]
         for i in range(m):
             for j in range(n):
@@ -73,7 +85,7 @@ def written_mask(case, lab, per, cn, status):
         for j in range(m):
             for i in range(j, m):
                 mask[eo(p["di"] + i, p["dj"] + j)] = True
-    elif op == "potrf_l":
+    elif op in ("potrf_l", "syrk_potrf_ln"):
         m, n = p["m"], p["n"]
         for j in range(n):
             for i in range(j, m):

@@ -78,6 +78,19 @@ def run_product(case, mats):
     if op == "potrf_l":
         return level3.potrf_l(p["m"], mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]), n=p["n"],
                               check=False)
+    if op == "gemm_nn":
+        level3.gemm_nn(p["m"], p["n"], p["k"], p["alpha"], mats["A"].ref(p["ai"], p["aj"]),
+                       mats["B"].ref(p["bi"], p["bj"]), p["beta"], mats["C"].ref(p["ci"], p["cj"]),
+                       mats["D"].ref(p["di"], p["dj"]))
+        return None
+    if op == "trmm_rlnn":
+        level3.trmm_rlnn(p["m"], p["n"], p["alpha"], mats["A"].ref(p["ai"], p["aj"]),
+                         mats["B"].ref(p["bi"], p["bj"]), mats["D"].ref(p["di"], p["dj"]))
+        return None
+    if op == "syrk_potrf_ln":
+        return level3.syrk_potrf_ln(p["m"], p["k"], mats["A"].ref(p["ai"], p["aj"]), mats["B"].ref(p["bi"], p["bj"]),
+                                    mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]), n=p["n"],
+                                    check=False)
     raise ValueError(op)
 
 
@@ -108,7 +121,7 @@ def test_golden_cases(batch):
             got = host(dm[lab])[:, : want.size]
             h = hm[lab]
             mask = written_mask(case, lab, want.size, h.cn, case["status"])
-            if case["op"] == "potrf_l" and lab == case["alias"].get("D", "D"):
+            if case["op"] in ("potrf_l", "syrk_potrf_ln") and lab == case["alias"].get("D", "D"):
                 mask[h.diag_off + case["params"]["dj"]: h.diag_off + case["params"]["dj"] + case["params"]["n"]] = True
             for b in range(batch):
                 compare_storage(got[b], want, mask, dims_n(case), f"{case['name']}/{lab}/item{b}")
@@ -589,3 +602,169 @@ def test_composite_kkt_schur_and_block_tridiag_vs_oracle():
         composite.block_tridiag_chol_factor(N, [pack.panel_from_array(x) for x in bad],
                                             [pack.panel_from_array(x) for x in E])
     assert ei.value.batch_index == 3 and ei.value.index == 2
+
+
+# ---------------------------------------------------------------------------
+# §8f next tier: gemm_nn, trmm_rlnn, syrk_potrf_ln, batched Riccati recursion
+
+NN_SHAPES = [(4, 4, 4), (8, 8, 8), (16, 16, 16), (24, 24, 24), (3, 17, 5), (28, 28, 28), (32, 32, 32),
+             (44, 36, 52), (64, 64, 64), (100, 100, 100), (128, 128, 128), (65, 130, 7), (9, 70, 33), (200, 40, 96)]
+
+
+def window_mask(h, o, m, n, lower=False):
+    mask = np.zeros(h.per, dtype=bool)
+    for j in range(n):
+        for i in range(j if lower else 0, m):
+            mask[O.element_offset(o[0] + i, o[1] + j, h.cn)] = True
+    return mask
+
+
+@pytest.mark.parametrize("mnk", NN_SHAPES)
+def test_gemm_nn_random_vs_oracle(mnk):
+    m, n, k = mnk
+    rng = np.random.default_rng(m * 7919 + n * 13 + k)
+    nb = 3 if m >= 128 else 11
+    for (oa, ob, oc, od, alpha, beta) in [((0, 0), (0, 0), (0, 0), (0, 0), 1.0, 1.0),
+                                          ((3, 1), (1, 2), (2, 0), (1, 3), -1.5, 0.5),
+                                          ((4, 0), (2, 4), (0, 0), (4, 1), 1.0, 0.0)]:
+        A = rand_batch(rng, nb, oa[0] + m + 1, oa[1] + k + 2)
+        B = rand_batch(rng, nb, ob[0] + k + 2, ob[1] + n + 1)
+        C = rand_batch(rng, nb, oc[0] + m, oc[1] + n)
+        D = rand_batch(rng, nb, od[0] + m + 3, od[1] + n + 1)
+        dA, dB, dC, dD = dev(A), dev(B), dev(C), dev(D)
+        level3.gemm_nn(m, n, k, alpha, dA.ref(*oa), dB.ref(*ob), beta, dC.ref(*oc), dD.ref(*od))
+        O.gemm_nn(m, n, k, alpha, A, *oa, B, *ob, beta, C, *oc, D, *od)
+        compare_storage(host(dD), D.storage, window_mask(D, od, m, n), max(m, n, k), f"gemm_nn {mnk} {oa}{od}")
+
+
+@pytest.mark.parametrize("mn", [(4, 4), (9, 6), (8, 8), (13, 7), (24, 24), (30, 20), (40, 40), (72, 48), (33, 70),
+                                (128, 128), (64, 200), (300, 96)])
+def test_trmm_rlnn_random_vs_oracle(mn):
+    m, n = mn
+    rng = np.random.default_rng(m * 131 + n)
+    nb = 3 if max(m, n) >= 128 else 9
+    for (oa, ob, od, alpha) in [((0, 0), (0, 0), (0, 0), 1.0), ((3, 2), (1, 1), (2, 3), -0.5),
+                                ((4, 4), (4, 0), (0, 4), 2.0)]:
+        T = rand_batch(rng, nb, oa[0] + n + 1, oa[1] + n + 2)
+        for i in range(n):  # poison the strict upper triangle: must never be read
+            for j in range(i + 1, n):
+                T.storage[:, O.element_offset(oa[0] + i, oa[1] + j, T.cn)] = np.nan
+        X = rand_batch(rng, nb, ob[0] + m + 2, ob[1] + n + 1)
+        D = rand_batch(rng, nb, od[0] + m + 1, od[1] + n + 1)
+        dT, dX, dD = dev(T), dev(X), dev(D)
+        level3.trmm_rlnn(m, n, alpha, dT.ref(*oa), dX.ref(*ob), dD.ref(*od))
+        O.trmm_rlnn(m, n, alpha, T, *oa, X, *ob, D, *od)
+        compare_storage(host(dD), D.storage, window_mask(D, od, m, n), max(m, n), f"trmm {mn} {oa}{od}")
+
+
+@pytest.mark.parametrize("mn", [(8, 8), (40, 40), (64, 100)])
+def test_trmm_in_place_matches_out_of_place(mn):
+    m, n = mn
+    rng = np.random.default_rng(5)
+    T = rand_batch(rng, 4, n, n)
+    X = rand_batch(rng, 4, m, n)
+    dT, dX, dY = dev(T), dev(X), dev(X)
+    out = dev(O.HostBatch(4, m, n))
+    level3.trmm_rlnn(m, n, 1.0, dT, dX, out)
+    level3.trmm_rlnn(m, n, 1.0, dT, dY, dY)
+    data = ((m + 3) // 4 * 4) * ((n + 3) // 4 * 4)  # data part; diag_inv is not written
+    assert np.array_equal(host(out)[:, :data].view(np.uint64), host(dY)[:, :data].view(np.uint64))
+
+
+@pytest.mark.parametrize("mkn", [(4, 3, None), (8, 8, None), (13, 5, None), (24, 16, None), (40, 33, None),
+                                 (64, 64, None), (100, 40, None), (136, 16, None), (20, 7, 12), (70, 9, 33)])
+def test_syrk_potrf_ln_random_vs_oracle(mkn):
+    m, k, n = mkn
+    n = m if n is None else n
+    rng = np.random.default_rng(m * 17 + k)
+    nb = 5
+    for (oa, oc, od) in [((0, 0), (0, 0), (0, 0)), ((1, 2), (3, 1), (4, 0)), ((0, 0), (0, 0), (2, 2))]:
+        A = rand_batch(rng, nb, oa[0] + m + 1, oa[1] + k + 1)
+        C = rand_batch(rng, nb, oc[0] + m + 1, oc[1] + n + 1)
+        for b in range(nb):
+            g = rng.uniform(-1, 1, (n, n))
+            spd = g @ g.T + n * np.eye(n)
+            for i in range(n):
+                for j in range(n):
+                    C.storage[b, O.element_offset(oc[0] + i, oc[1] + j, C.cn)] = spd[i, j]
+        D = rand_batch(rng, nb, od[0] + m + 2, od[1] + n + 1)
+        dA, dC, dD = dev(A), dev(C), dev(D)
+        info = level3.syrk_potrf_ln(m, k, dA.ref(*oa), dA.ref(*oa), dC.ref(*oc), dD.ref(*od), n=n)
+        oinfo = O.syrk_potrf_ln(m, k, A, *oa, A, *oa, C, *oc, D, *od, n=n)
+        assert np.array_equal(info.cpu().numpy(), oinfo)
+        mask = window_mask(D, od, m, n, lower=True)
+        mask[D.diag_off + od[1]: D.diag_off + od[1] + n] = True
+        compare_storage(host(dD), D.storage, mask, max(m, k), f"syrk_potrf {mkn} {oa}{od}")
+        assert (dD.diag_lo, dD.diag_hi) == (D.diag_lo, D.diag_hi)
+
+
+def test_syrk_potrf_failure_and_k0_rules():
+    rng = np.random.default_rng(3)
+    m, k = 12, 4
+    A = rand_batch(rng, 3, m, k)
+    C = O.HostBatch(3, m, m)
+    for b in range(3):
+        g = rng.uniform(-1, 1, (m, m))
+        C.set_window(0, 0, np.broadcast_to(g @ g.T + m * np.eye(m), (3, m, m)))
+    C.storage[1, O.element_offset(7, 7, C.cn)] = -1e4  # item 1 fails at pivot 7
+    D = rand_batch(rng, 3, m, m)
+    dA, dC, dD = dev(A), dev(C), dev(D)
+    with pytest.raises(pb.NotPositiveDefiniteError) as ei:
+        level3.syrk_potrf_ln(m, k, dA, dA, dC, dD)
+    assert ei.value.index == 7 and ei.value.batch_index == 1
+    oinfo = O.syrk_potrf_ln(m, k, A, 0, 0, A, 0, 0, C, 0, 0, D, 0, 0)
+    assert list(oinfo) == [-1, 7, -1]
+    mask = window_mask(D, (0, 0), m, m, lower=True)
+    mask[D.diag_off: D.diag_off + m] = True
+    compare_storage(host(dD), D.storage, mask, m, "syrk_potrf failure partial writes")
+    # k = 0 (and zero factors) reduce to plain potrf_l, bit-equal (test_level3.py:343-353, 632-641)
+    d1, d2 = dev(O.HostBatch(3, m, m)), dev(O.HostBatch(3, m, m))
+    C.storage[1, O.element_offset(7, 7, C.cn)] = C.storage[0, O.element_offset(7, 7, C.cn)]
+    dC = dev(C)
+    level3.syrk_potrf_ln(m, 0, dA, dA, dC, d1)
+    level3.potrf_l(m, dC, d2)
+    assert np.array_equal(host(d1).view(np.uint64), host(d2).view(np.uint64))
+
+
+def _riccati_golden_inputs(z, r, batch):
+    nx, nu, N = r["nx"], r["nu"], r["N"]
+    ns = nx + nu
+    rep = lambda a: torch.from_numpy(np.repeat(a[None, :], batch, axis=0)).cuda()  # noqa: E731
+    bat = [pb.create_panel_batch(batch, ns, nx, rep(z[f"{r['key']}/bat{n}"])) for n in range(N)]
+    rsq = [pb.create_panel_batch(batch, ns, ns, rep(z[f"{r['key']}/rsq{n}"])) for n in range(N)]
+    P = pb.create_panel_batch(batch, nx, nx, rep(z[f"{r['key']}/P"]))
+    return bat, rsq, P
+
+
+@pytest.mark.parametrize("batch", [1, 6])
+def test_riccati_factorize_golden(batch):
+    """Batched composite.riccati_factorize against the reference's own
+    apps.riccati_factorize outputs (tests/golden, apps.py:231-254)."""
+    from paper_1704_02457_b200 import composite
+    z, _ = load_golden()
+    import json
+    rics = json.loads(str(z["manifest"]))["riccati"]
+    assert len(rics) >= 4
+    for r in rics:
+        nx, nu, N = r["nx"], r["nu"], r["N"]
+        ns = nx + nu
+        bat, rsq, P = _riccati_golden_inputs(z, r, batch)
+        if r["status"] >= 0:
+            with pytest.raises(pb.FactorizationError) as ei:
+                composite.riccati_factorize(nx, nu, N, bat, rsq, P)
+            assert str(ei.value).startswith(r["msg"].split(":")[0] + ":"), (str(ei.value), r["msg"])
+            assert ei.value.index == r["status"]
+            continue
+        ws = composite.riccati_factorize(nx, nu, N, bat, rsq, P)
+        torch.cuda.synchronize()
+        for n in range(N):
+            want = z[f"{r['key']}/F{n}"]
+            got = host(ws.factors[n])[:, : want.size]
+            h = O.HostBatch(1, ns, ns)
+            mask = np.zeros(want.size, dtype=bool)
+            for j in range(ns):
+                for i in range(j, ns):
+                    mask[O.element_offset(i, j, h.cn)] = True
+            mask[h.diag_off: h.diag_off + ns] = True
+            for b in range(batch):
+                compare_storage(got[b], want, mask, ns, f"{r['name']} stage {n} item {b}")

@@ -97,7 +97,7 @@ def _header_symbols():
 def test_native_library_exports_header_surface():
     lib = _native.load()
     syms = _header_symbols()
-    assert len(syms) == 13, syms
+    assert len(syms) == 16, syms
     assert set(syms) == set(_native.SIGNATURES)
     for s in syms:
         assert hasattr(lib, s), s

@@ -40,7 +40,7 @@ def test_golden_cases_bit_exact():
             want = z[f"{case['key']}/out/{lab}"]
             got = mats[lab].storage[0, : want.size]
             assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (case["name"], lab)
-        if case["op"] == "potrf_l":
+        if case["op"] in ("potrf_l", "syrk_potrf_ln"):
             d = mats[case["alias"].get("D", "D")]
             assert [d.diag_lo, d.diag_hi] == case["valid_out"]["D"], case["name"]
 
@@ -167,3 +167,93 @@ def test_oracle_chain_matches_dense_riccati():
     Pd = dense_riccati(A, B, Q, R, 12)
     Pfull = np.tril(P) + np.tril(P, -1).transpose(0, 2, 1)
     assert np.max(np.abs(Pfull - Pd)) / np.max(np.abs(Pd)) < 1e-12
+
+
+@pytest.mark.skipif(ref_core is None, reason="oracle/_ref not built (make -C oracle ref)")
+def test_oracle_next_tier_matches_compiled_reference_core():
+    """gemm_nn, trmm_rlnn and the fused syrk_potrf
+    restated in pb_oracle.c are bit-identical to the reference's own core."""
+    rng = np.random.default_rng(17)
+    P = O.ctypes.c_void_p
+    for trial in range(25):
+        m, n, k = (int(x) for x in rng.integers(1, 30, 3))
+        sd = 4 * ((max(m, n, k) + 3) // 4) + 8
+        rows = sd
+        A, B, C = (rng.standard_normal(rows * sd) for _ in range(3))
+        D1 = rng.standard_normal(rows * sd)
+        D2 = D1.copy()
+        ci, di, bi = int(rng.integers(0, 4)), int(rng.integers(0, 4)), int(rng.integers(0, 4))
+        alpha, beta = float(rng.choice([1.0, -0.5, 0.0])), float(rng.choice([0.0, 2.0]))
+        ref_core.gemm_nn_drv(m, n, k, alpha, A, 0, 1, sd, B, bi, 2, sd, beta, C, ci, 0, sd, D1, di, 1, sd)
+        O.lib().po_gemm_nn(*[O._L(x) for x in (m, n, k)], O._D(alpha), A.ctypes.data_as(P), O._L(0), O._L(1),
+                           O._L(sd), B.ctypes.data_as(P), O._L(bi), O._L(2), O._L(sd), O._D(beta),
+                           C.ctypes.data_as(P), O._L(ci), O._L(0), O._L(sd), D2.ctypes.data_as(P), O._L(di),
+                           O._L(1), O._L(sd))
+        assert np.array_equal(D1.view(np.uint64), D2.view(np.uint64)), ("gemm_nn", trial)
+        # trmm_rlnn: X m x n, T n x n lower (strict upper poisoned: never read)
+        T = rng.standard_normal(rows * sd)
+        for i in range(n):
+            for j in range(i + 1, n):
+                T[O.element_offset(i, j, sd)] = np.nan
+        ti = int(rng.integers(0, 4))
+        for i in range(n):
+            for j in range(i + 1, n):
+                T[O.element_offset(ti + i, j, sd)] = np.nan
+        E1 = rng.standard_normal(rows * sd)
+        E2 = E1.copy()
+        ref_core.trmm_rlnn_drv(m, n, alpha, A, 0, 0, sd, T, ti, 0, sd, E1, di, 0, sd)
+        O.lib().po_trmm_rlnn(O._L(m), O._L(n), O._D(alpha), T.ctypes.data_as(P), O._L(ti), O._L(0), O._L(sd),
+                             A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), E2.ctypes.data_as(P), O._L(di),
+                             O._L(0), O._L(sd))
+        assert np.array_equal(E1.view(np.uint64), E2.view(np.uint64)), ("trmm", trial)
+        # syrk_potrf: C + A A^T with C = g g^T + shift (SPD), tall when m > n
+        nn = min(n, m)
+        g = rng.uniform(-1, 1, (m, m))
+        spd = g @ g.T + m * np.eye(m)
+        Cs = np.zeros(rows * sd)
+        for i in range(m):
+            for j in range(nn):
+                Cs[O.element_offset(i, j, sd)] = spd[i, j]
+        F1 = np.full(rows * sd, 3.0)
+        F2 = F1.copy()
+        v1, v2 = np.zeros(sd), np.zeros(sd)
+        st1 = ref_core.syrk_potrf_drv(m, nn, k, A, 0, 0, sd, A, 0, 0, sd, Cs, 0, 0, sd, F1, 0, 0, sd, v1, 0)
+        st2 = O.lib().po_syrk_potrf_ln(O._L(m), O._L(nn), O._L(k), A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                                       A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), Cs.ctypes.data_as(P), O._L(0),
+                                       O._L(0), O._L(sd), F2.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                                       v2.ctypes.data_as(P), O._L(0))
+        assert st1 == st2, trial
+        assert np.array_equal(F1.view(np.uint64), F2.view(np.uint64)), ("syrk_potrf", trial)
+        assert np.array_equal(v1.view(np.uint64), v2.view(np.uint64)), ("syrk_potrf dinv", trial)
+
+
+def test_oracle_riccati_composition_bit_exact_vs_reference_golden():
+    """The oracle's trmm_rlnn + syrk_potrf_ln, composed as apps.riccati_factorize
+    (apps.py:218-254), reproduce the reference's stage factors bit for bit."""
+    import json
+    z, _ = load_golden()
+    rics = json.loads(str(z["manifest"]))["riccati"]
+    for r in rics:
+        nx, nu, N = r["nx"], r["nu"], r["N"]
+        ns = nx + nu
+        term = O.HostBatch(1, nx, nx)
+        P = O.HostBatch(1, nx, nx, z[f"{r['key']}/P"][None, :].copy())
+        info = O.potrf_l(nx, P, 0, 0, term, 0, 0)
+        assert info[0] < 0
+        lnext, li = term, 0
+        failed = -1
+        for n in range(N - 1, -1, -1):
+            bat = O.HostBatch(1, ns, nx, z[f"{r['key']}/bat{n}"][None, :].copy())
+            rsq = O.HostBatch(1, ns, ns, z[f"{r['key']}/rsq{n}"][None, :].copy())
+            cbuf, F = O.HostBatch(1, ns, nx), O.HostBatch(1, ns, ns)
+            O.trmm_rlnn(ns, nx, 1.0, lnext, li, li, bat, 0, 0, cbuf, 0, 0)
+            st = O.syrk_potrf_ln(ns, nx, cbuf, 0, 0, cbuf, 0, 0, rsq, 0, 0, F, 0, 0)[0]
+            if st >= 0:
+                failed = st
+                assert r["msg"].startswith(f"stage {n}:"), r
+                break
+            if r["status"] < 0:  # the reference keeps factors only for a completed sweep
+                want = z[f"{r['key']}/F{n}"]
+                assert np.array_equal(F.storage[0, : want.size].view(np.uint64), want.view(np.uint64)), (r["name"], n)
+            lnext, li = F, nu
+        assert failed == r["status"], r["name"]
