@@ -84,6 +84,24 @@ class Point:
             self.flops_item = float(m) * n * n
             self.bytes_item = 8.0 * (n * (n + 1) / 2 + n + 2 * m * n)
             self.io_bytes = memsize(n, n) + 2 * memsize(m, n)
+        elif op == "gemm_nn":
+            self.flops_item = 2.0 * m * n * k
+            self.bytes_item = 8.0 * (m * k + n * k + (m * n if beta != 0 else 0) + m * n)
+            self.io_bytes = memsize(m, k) + memsize(k, n) + (memsize(m, n) if beta != 0 else 0) + memsize(m, n)
+        elif op == "trmm_rlnn":  # reference flop_count (bench.py:90-91)
+            self.flops_item = float(m) * n * n
+            self.bytes_item = 8.0 * (n * (n + 1) / 2 + 2 * m * n)
+            self.io_bytes = memsize(n, n) + 2 * memsize(m, n)
+        elif op == "syrk_potrf_ln":  # m x m, A = B (m x k); bench.py:94-95
+            self.flops_item = float(m) * (m + 1) * k + m ** 3 / 3.0
+            self.bytes_item = 8.0 * (m * k + m * (m + 1) + m)
+            self.io_bytes = memsize(m, k) + 2 * memsize(m, m)
+        elif op == "riccati_fact":  # apps.riccati_factorize: m = nx, n = nu, k = N; bench.py:98-101
+            nx, nu, ns = m, n, m + n
+            self.flops_item = k * (float(ns) * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0)
+            # per stage: read [B';A'], L_next (lower), [R S;S' Q] (lower); write cbuf, read it back; write F + diag_inv
+            self.bytes_item = k * 8.0 * (3 * ns * nx + nx * (nx + 1) / 2 + ns * (ns + 1) + ns)
+            self.io_bytes = (k + 1) * (memsize(ns, nx) + 2 * memsize(ns, ns))
         elif op == "riccati":  # m = nx, n = nu, k = N stages
             nx, nu, ns = m, n, m + n
             per_stage = (2.0 * ns * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0 + float(nx) * nu * nu
@@ -99,6 +117,10 @@ class Point:
 
     @property
     def label(self):
+        if self.op == "riccati_fact":
+            return f"riccati_factorize nx={self.m} nu={self.n} N={self.k}"
+        if self.op in ("gemm_nn", "syrk_potrf_ln"):
+            return f"{self.op} {self.m}x{self.n}x{self.k}"
         if self.op == "riccati":
             return f"riccati nx={self.m} nu={self.n} N={self.k}"
         if self.op == "potrf_l":
@@ -128,6 +150,11 @@ def config_points(name):
     if name == "c5":
         return [Point("riccati", 32, 8, 50, 1024)], \
             "C5 Riccati-style chain: 1024 problems x N=50 stages, nx=32 nu=8 (gemm_nt, syrk_ln, potrf_l, trsm_rltn, gemm_nt per stage)"
+    if name == "c6":
+        return [Point("gemm_nn", 64, 64, 64, 4096, 1.0, 1.0), Point("trmm_rlnn", 40, 32, 0, 16384, 1.0),
+                Point("syrk_potrf_ln", 40, 40, 32, 16384), Point("riccati_fact", 32, 8, 50, 1024)], \
+            ("C6 next tier (SURVEY §8f): dgemm_nn 64^3 batch 4096, dtrmm_rlnn 40x32 and dsyrk_potrf_ln 40x40 k=32 "
+             "batch 16384, apps.riccati_factorize nx=32 nu=8 N=50 x 1024 problems")
     raise SystemExit(f"unknown config {name}")
 
 
@@ -205,6 +232,53 @@ class GpuPoint:
             if not self.fused:
                 ch.capture(k)
             self.chain = ch
+        elif pt.op == "gemm_nn":
+            self.A = pb.allocate_panel_batch(nb, m, k, device=device)
+            self.B = pb.allocate_panel_batch(nb, k, n, device=device)
+            self.C = pb.allocate_panel_batch(nb, m, n, device=device)
+            for x in (self.A, self.B, self.C):
+                x.storage.uniform_(-1, 1, generator=g)
+            self.D = pb.allocate_panel_batch(nb, m, n, device=device, zero=True)
+        elif pt.op == "trmm_rlnn":
+            self.A = pb.allocate_panel_batch(nb, n, n, device=device)
+            self.A.storage.uniform_(-1, 1, generator=g)
+            self.B = pb.allocate_panel_batch(nb, m, n, device=device)
+            self.B.storage.uniform_(-1, 1, generator=g)
+            self.D = pb.allocate_panel_batch(nb, m, n, device=device, zero=True)
+        elif pt.op == "syrk_potrf_ln":
+            self.A = pb.allocate_panel_batch(nb, m, k, device=device)
+            self.A.storage.uniform_(-1, 1, generator=g)
+            self.C = pb.allocate_panel_batch(nb, m, m, device=device)
+            Md = u(nb, m, m)
+            pack.pack_array_into(torch.baddbmm(torch.eye(m, dtype=torch.float64, device=device).expand(nb, m, m) * m,
+                                               Md, Md.transpose(1, 2)), self.C)
+            self.D = pb.allocate_panel_batch(nb, m, m, device=device, zero=True)
+        elif pt.op == "riccati_fact":
+            from paper_1704_02457_b200 import composite
+            nx, nu, N = m, n, k
+            ns = nx + nu
+            self.bat, self.rsq = [], []
+            for _ in range(N):
+                Ad = u(nb, nx, nx) * 0.5 + 0.8 * torch.eye(nx, dtype=torch.float64, device=device)
+                Bd = u(nb, nx, nu)
+                self.bat.append(pack.panel_from_array(torch.cat([Bd.transpose(1, 2), Ad.transpose(1, 2)], 1)
+                                                      .contiguous()))
+                Gd = u(nb, ns, ns)
+                self.rsq.append(pack.panel_from_array(
+                    torch.baddbmm(torch.eye(ns, dtype=torch.float64, device=device).expand(nb, ns, ns) * ns,
+                                  Gd, Gd.transpose(1, 2))))
+            Gp = u(nb, nx, nx)
+            self.Pn = pack.panel_from_array(torch.baddbmm(torch.eye(nx, dtype=torch.float64, device=device)
+                                                          .expand(nb, nx, nx) * nx, Gp, Gp.transpose(1, 2)))
+            self.ws = composite.RiccatiBatchWorkspace(nb, nx, nu, N, device=device)
+            composite.riccati_factorize(nx, nu, N, self.bat, self.rsq, self.Pn, workspace=self.ws)  # checked once
+            torch.cuda.synchronize()
+            _native_mod = __import__("paper_1704_02457_b200._native", fromlist=["launch_count"])
+            c0 = _native_mod.launch_count()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                composite.riccati_factorize(nx, nu, N, self.bat, self.rsq, self.Pn, workspace=self.ws, check=False)
+            self.graph_kernels = _native_mod.launch_count() - c0
         elif pt.op == "trsm_rltn":
             from paper_1704_02457_b200 import level3
             M = u(nb, n, n)
@@ -239,6 +313,15 @@ class GpuPoint:
                 level3.syrk_ln(pt.m, pt.k, pt.alpha, a, a, pt.beta, self.C, self.D)
             elif pt.op == "trsm_rltn":
                 level3.trsm_rltn(pt.m, pt.n, pt.alpha, self.A, self.B, self.D, check=False)
+            elif pt.op == "gemm_nn":
+                level3.gemm_nn(pt.m, pt.n, pt.k, pt.alpha, self.A, self.B, pt.beta, self.C, self.D)
+            elif pt.op == "trmm_rlnn":
+                level3.trmm_rlnn(pt.m, pt.n, pt.alpha, self.A, self.B, self.D)
+            elif pt.op == "syrk_potrf_ln":
+                level3.syrk_potrf_ln(pt.m, pt.k, self.A, self.A, self.C, self.D, check=False)
+            elif pt.op == "riccati_fact":
+                self.graph.replay()  # whole backward sweep: one graph of trmm + syrk/gemm + potrf per stage
+                GRAPH_LAUNCHES[0] += self.graph_kernels
             elif pt.op == "riccati":
                 # P_N = Q, then the captured N-stage sweep (one graph launch of 5N kernels)
                 self.chain.P.storage.copy_(self.Q.storage)
@@ -584,13 +667,53 @@ def _cpu_worker(job):
         flops_item = N * (2.0 * ns * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0 + float(nx) * nu * nu
                           + 2.0 * nx * nx * nx)
         Cs = [None]
+    elif op == "riccati_fact":
+        nx, nu, N = m, n, k
+        ns = nx + nu
+        sdx, sds = -(-nx // 4) * 4, -(-ns // 4) * 4
+        rs = -(-ns // 4) * 4
+        bats = [rng.uniform(-1, 1, rs * sdx) for _ in range(4)]
+        RSQ = np.zeros(rs * sds)
+        ii = np.arange(ns)
+        RSQ[(ii - (ii & 3)) * sds + 4 * ii + (ii & 3)] = 1.0 + ns
+        Lt = np.zeros(sdx * sdx)
+        Lt[(np.arange(nx) - (np.arange(nx) & 3)) * sdx + 4 * np.arange(nx) + (np.arange(nx) & 3)] = 1.0
+        cb = np.zeros(rs * sdx)
+        Fs = [np.zeros(rs * sds) for _ in range(N)]
+        dv = np.zeros(ns)
+
+        def call(c):  # apps.riccati_step x N (apps.py:218-228) through the core drivers
+            Tm, to = Lt, 0
+            for st in range(N - 1, -1, -1):
+                core.trmm_rlnn_drv(ns, nx, 1.0, bats[st & 3], 0, 0, sdx, Tm, to, to, sdx if to == 0 else sds,
+                                   cb, 0, 0, sdx)
+                core.syrk_potrf_drv(ns, ns, nx, cb, 0, 0, sdx, cb, 0, 0, sdx, RSQ, 0, 0, sds, Fs[st], 0, 0, sds, dv, 0)
+                Tm, to = Fs[st], nu
+        flops_item = N * (float(ns) * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0)
+        Cs = [None]
     else:
         sdk = -(-k // 4) * 4 if op != "trsm_rltn" else cn
         A = rng.uniform(-1, 1, ru(m + 4) * max(sdk, cn, 4) + 64)
         B = rng.uniform(-1, 1, ru(max(m, n) + 4) * max(sdk, cn, 4) + 64)
         Cm = rng.uniform(-1, 1, ru(m + 4) * max(cn, ru(m)) + 64)
         D = np.zeros_like(Cm)
-        if op == "gemm_nt":
+        if op == "gemm_nn":
+            call = lambda c: core.gemm_nn_drv(m, n, k, alpha, A, 0, 0, sdk, B, 0, 0, cn, beta, Cm, 0, 0, cn,  # noqa: E731
+                                              D, 0, 0, cn)
+            flops_item = 2.0 * m * n * k
+        elif op == "trmm_rlnn":
+            call = lambda c: core.trmm_rlnn_drv(m, n, alpha, B, 0, 0, cn, A, 0, 0, cn, D, 0, 0, cn)  # noqa: E731
+            flops_item = float(m) * n * n
+        elif op == "syrk_potrf_ln":
+            cm = ru(m)
+            Cm[:] = 0.0
+            ii = np.arange(m)
+            Cm[(ii - (ii & 3)) * cm + 4 * ii + (ii & 3)] = 1.0 + m * k
+            dvv = np.zeros(m)
+            call = lambda c: core.syrk_potrf_drv(m, m, k, A, 0, 0, sdk, A, 0, 0, sdk, Cm, 0, 0, cm,  # noqa: E731
+                                                 D, 0, 0, cm, dvv, 0)
+            flops_item = float(m) * (m + 1) * k + m ** 3 / 3.0
+        elif op == "gemm_nt":
             call = lambda c: core.gemm_nt_drv(m, n, k, alpha, A, 0, 0, sdk, B, 0, 0, sdk, beta, Cm, 0, 0, cn,  # noqa: E731
                                               D, 0, 0, cn)
             flops_item = 2.0 * m * n * k

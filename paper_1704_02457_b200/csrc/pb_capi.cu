@@ -335,6 +335,28 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
   if (!sD->dA) return fail_arg(13, "output needs diag_inv storage");
   if (!info) return fail_arg(16, "info is required");
   cudaStream_t st = (cudaStream_t)stream;
+  // k == 0: exactly potrf_l of C (test_level3.py:343-353)
+  if (k == 0) return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, st);
+  const bool ab_same = sA->pA == sB->pA && sA->stride == sB->stride && sA->cn == sB->cn && ai == bi && aj == bj;
+  // squares the register-resident small potrf covers keep its rounding
+  // (zero factors then reproduce potrf_l bit for bit, test_level3.py:632-641)
+  const bool small = m == n && n <= 16 && (di & 3) == 0 && tma_ok(sD);
+  if (!small && syrk_potrf_fits(m, n, k, ab_same)) {
+    // one fused kernel: the item's C tri, A and B windows in shared memory
+    PotrfArgs g;
+    g.m = m, g.n = n;
+    g.C = to_mat(sC), g.D = to_mat(sD);
+    g.ci = ci, g.cj = cj, g.di = di, g.dj = dj;
+    g.info = info;
+    g.batch = batch;
+    g.merge = 0;
+    g.info_offset = 0;
+    g.syrk = 1;
+    g.ab_same = ab_same;
+    g.A = to_mat(sA), g.B = to_mat(sB);
+    g.ai = ai, g.aj = aj, g.bi = bi, g.bj = bj, g.k = k;
+    return finish(run_syrk_potrf(g, st));
+  }
   // W = lower trapezoid of C + A*B^T in a stream-ordered workspace, then
   // potrf_l(W -> D).  syrk_potrf_drv (ccore.pyx:908-941) walks the same
   // block rows as potrf_drv with the tile input C + A*B^T, so D's contents

@@ -54,10 +54,35 @@ __device__ __forceinline__ void tri_load(double *S, const Tri &t, const double *
   }
 }
 
+// Stage a rows x k window (rows padded to rpad with zeros, columns to kp)
+// into a plain panel-major buffer of panel length kp.
+__device__ __forceinline__ void panel_load(double *S, int kp, const double *X, ix cn, ix xi, ix xj, int rows, int rpad,
+                                           int k, int ttid, int tthreads) {
+  const bool vec = (xi & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  if (vec) {
+    for (int q = ttid; q < (rpad / 4) * kp * 2; q += tthreads) {
+      const int p = q / (2 * kp), w = q % (2 * kp), l = w >> 1, h = w & 1;
+      const int r = 4 * p + 2 * h;
+      const bool ok = r < rows && l < k;  // rows come in pairs: rows, k are whole-panel padded below
+      const double *src = ok ? X + eo(xi + r, xj + l, cn) : X;
+      cp_async16(S + p * 4 * kp + 4 * l + 2 * h, src, ok ? 16 : 0);
+    }
+  } else {
+    for (int q = ttid; q < rpad * kp; q += tthreads) {
+      const int p = q / (4 * kp), w = q % (4 * kp), l = w >> 2, rr = w & 3;
+      const int r = 4 * p + rr;
+      S[q] = (r < rows && l < k) ? X[eo(xi + r, xj + l, cn)] : 0.0;
+    }
+  }
+}
+
 // GM/GN > 0 fix the row/column group counts at compile time (the common
 // square sizes): every tile loop then unrolls and all tri-layout offsets
 // fold to constants; GM = GN = 0 is the generic runtime-shaped kernel.
-template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0>
+// SK: fused syrk_potrf -- the item's A (and B) windows sit next to the tri
+// buffer and every tile's downdate also accumulates + A_g B_j^T, exactly
+// the per-tile order of syrk_potrf_drv (ccore.pyx:908-941).
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false>
 __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -76,6 +101,10 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   double *dinv = S0 + (DB ? 2 : 1) * tri_elems;         // cn8 doubles
   volatile int *flag = (volatile int *)(dinv + t.cn8);  // failure index
   double *Wp = dinv + t.cn8 + 8;                        // inverted diagonal block (64)
+  // SK operands: A rows padded to 8*gm, B rows to 8*gn, panel length kp
+  const int kp = SK ? (int)((g.k + 3) & ~(ix)3) : 0;
+  double *SA = Wp + 64;
+  double *SB = SK && !g.ab_same ? SA + 8 * gm * kp : SA;
   const int fr = lane >> 2, fc = lane & 3;
   const bool aligned_out = (g.di & 3) == 0;
   const bool vin = vec_in != 0;
@@ -84,7 +113,16 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   auto skip = [&](ix b) { return g.merge && g.info[b] >= 0; };
   ix b = (ix)blockIdx.x * teams_per_cta + team;
   while (b < g.batch && skip(b)) b += stride;
-  if (b < g.batch) tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+  auto stage_ab = [&](ix bb) {
+    if (SK) {
+      panel_load(SA, kp, g.A.item(bb), g.A.cn, g.ai, g.aj, m, 8 * gm, (int)g.k, ttid, tthreads);
+      if (!g.ab_same) panel_load(SB, kp, g.B.item(bb), g.B.cn, g.bi, g.bj, n, 8 * t.gn, (int)g.k, ttid, tthreads);
+    }
+  };
+  if (b < g.batch) {
+    tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+    stage_ab(b);
+  }
   cp_async_commit();
   int cur = 0;
   for (; b < g.batch;) {
@@ -114,6 +152,12 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
         if (gg < gm) {
           acc[u][0] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc)];
           acc[u][1] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc + 1)];
+          if (SK) {
+            const int pa = (2 * gg + (lane >> 4)) * 4 * kp + 4 * fc + (fr & 3);
+            const int pb = (2 * jb + (lane >> 4)) * 4 * kp + 4 * fc + (fr & 3);
+#pragma unroll 4
+            for (int kk = 0; kk < kp / 4; ++kk) dmma(acc[u], SA[pa + 16 * kk], SB[pb + 16 * kk]);
+          }
           const int fa = tri_frag(t, gg, 0, lane), fb = tri_frag(t, jb, 0, lane);
 #pragma unroll 4
           for (int kk = 0; kk < 2 * jb; ++kk) dmma(acc[u], -S[fa + 16 * kk], S[fb + 16 * kk]);
@@ -205,6 +249,7 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     if (DB && vin) cur ^= 1;
     else if (b < g.batch) {
       tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+      stage_ab(b);
       cp_async_commit();
     }
   }
@@ -311,11 +356,17 @@ static int pick_teams(int tw, ix team_elems, int &threads, size_t &smem) {
   return teams;
 }
 
-template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0>
+static ix syrk_operand_elems(ix m, ix n, ix k, bool ab_same) {
+  const ix kp = (k + 3) & ~(ix)3;
+  return (m + 7) / 8 * 8 * kp + (ab_same ? 0 : (n + 7) / 8 * 8 * kp);
+}
+
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false>
 static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
-  auto kern = potrf_team_kernel<TW, MAXT, DB, GM, GN>;
+  auto kern = potrf_team_kernel<TW, MAXT, DB, GM, GN, SK>;
   const ix cn8 = (g.n + 7) / 8 * 8;
-  ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8 + 64;
+  ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8 + 64 +
+                  (SK ? syrk_operand_elems(g.m, g.n, g.k, g.ab_same != 0) : 0);
   team_elems = (team_elems + 15) / 16 * 16;
   int threads;
   size_t smem;
@@ -358,6 +409,23 @@ cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   if (gm <= 16) return launch_potrf<8, 2, false>(g, st);
   if (gm <= 32) return launch_potrf<8, 4, false>(g, st);
   return launch_potrf<8, 8, false>(g, st);
+}
+
+bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same) {
+  const ix cn8 = (n + 7) / 8 * 8;
+  const ix e = Tri::size(m, n) + cn8 + 8 + 64 + syrk_operand_elems(m, n, k, ab_same);
+  return e * 8 <= 220 * 1024 && (m + 7) / 8 <= 8 * 8;
+}
+
+// fused syrk + potrf: single-buffered generic team shapes
+cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st) {
+  const ix gm = (g.m + 7) / 8;
+  if (gm <= 2) return launch_potrf<1, 2, false, 0, 0, true>(g, st);
+  if (gm <= 4) return launch_potrf<1, 4, false, 0, 0, true>(g, st);
+  if (gm <= 8) return launch_potrf<4, 2, false, 0, 0, true>(g, st);
+  if (gm <= 16) return launch_potrf<8, 2, false, 0, 0, true>(g, st);
+  if (gm <= 32) return launch_potrf<8, 4, false, 0, 0, true>(g, st);
+  return launch_potrf<8, 8, false, 0, 0, true>(g, st);
 }
 
 bool trsm_fits(ix m, ix n) {

@@ -37,6 +37,12 @@ struct PotrfArgs {
   // skipped; a new failure is stored as info_offset + local index.
   int merge;
   int info_offset;
+  // fused syrk_potrf (syrk_potrf_drv ccore.pyx:908-941): factor
+  // lower(C + A*B^T), A m x k, B n x k; B may be A's own window (ab_same)
+  int syrk = 0;
+  int ab_same = 0;
+  Mat A{}, B{};
+  ix ai = 0, aj = 0, bi = 0, bj = 0, k = 0;
 };
 
 struct CopyArgs {
@@ -65,6 +71,8 @@ cudaError_t run_unpack(const CopyArgs &g, cudaStream_t st);
 cudaError_t run_gecp(const CopyArgs &g, cudaStream_t st);
 cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *info, cudaStream_t st);
 bool potrf_fits(ix m, ix n);
+bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same);
+cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st);
 bool potrf_small_ok(const PotrfArgs &g);
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);

@@ -724,6 +724,15 @@ def test_syrk_potrf_failure_and_k0_rules():
     level3.syrk_potrf_ln(m, 0, dA, dA, dC, d1)
     level3.potrf_l(m, dC, d2)
     assert np.array_equal(host(d1).view(np.uint64), host(d2).view(np.uint64))
+    for mm in (12, 24, 40):  # small-kernel and team-kernel regimes
+        Cz = O.HostBatch(2, mm, mm)
+        g = rng.uniform(-1, 1, (mm, mm))
+        Cz.set_window(0, 0, np.broadcast_to(g @ g.T + mm * np.eye(mm), (2, mm, mm)))
+        dZ, dCz = dev(O.HostBatch(2, mm, 3)), dev(Cz)
+        e1, e2 = dev(O.HostBatch(2, mm, mm)), dev(O.HostBatch(2, mm, mm))
+        level3.syrk_potrf_ln(mm, 3, dZ, dZ, dCz, e1)
+        level3.potrf_l(mm, dCz, e2)
+        assert np.array_equal(host(e1), host(e2)), mm  # == (a zero product may flip -0 to +0)
 
 
 def _riccati_golden_inputs(z, r, batch):
