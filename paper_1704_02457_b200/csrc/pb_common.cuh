@@ -81,6 +81,16 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 1-D bulk copy shared -> global (bulk-group completion), bytes % 16 == 0.
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// wait until every committed bulk store has finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // Named barrier for a team of `nthreads` (multiple of 32) with id 1..15.

@@ -54,6 +54,39 @@ __device__ __forceinline__ void tri_load(double *S, const Tri &t, const double *
   }
 }
 
+// Bulk-copy variant of tri_load for panel-aligned, 16-byte aligned items:
+// every (row group, half) of the tri layout is ONE contiguous run of the
+// item's panel (4 rows x min(width, n) columns), so thread 0 issues one
+// cp.async.bulk per run (completion on the team's mbarrier) and the other
+// threads only zero the padding columns [n, width) and the rows past m.
+// Rows of a partial last panel are read as stored (they only ever feed
+// their own rows and are never written back).
+__device__ __forceinline__ void tri_load_bulk(double *S, const Tri &t, const double *C, ix cn, ix ci, ix cj, int m,
+                                              int n, int gm, uint64_t *tbar, int ttid, int tthreads) {
+  if (ttid == 0) {
+    unsigned bytes = 0;
+    for (int gg = 0; gg < gm; ++gg)
+      for (int h = 0; h < 2; ++h)
+        if (8 * gg + 4 * h < m) bytes += 32u * (unsigned)min(t.width(gg), n);
+    mbar_arrive_expect_tx(tbar, bytes);
+    for (int gg = 0; gg < gm; ++gg) {
+      const int w = t.width(gg), base = t.group_off(gg);
+      for (int h = 0; h < 2; ++h) {
+        const int r0 = 8 * gg + 4 * h;
+        if (r0 < m) tma_load_1d(S + base + h * 4 * w, C + eo(ci + r0, cj, cn), 32u * (unsigned)min(w, n), tbar);
+      }
+    }
+  }
+  for (int gg = 0; gg < gm; ++gg) {
+    const int w = t.width(gg), base = t.group_off(gg);
+    for (int h = 0; h < 2; ++h) {
+      const int r0 = 8 * gg + 4 * h;
+      const int c0 = r0 < m ? min(w, n) : 0;
+      for (int q = ttid; q < 4 * (w - c0); q += tthreads) S[base + h * 4 * w + 4 * c0 + q] = 0.0;
+    }
+  }
+}
+
 // Stage a rows x k window (rows padded to rpad with zeros, columns to kp)
 // into a plain panel-major buffer of panel length kp.
 __device__ __forceinline__ void panel_load(double *S, int kp, const double *X, ix cn, ix xi, ix xj, int rows, int rpad,
@@ -76,14 +109,97 @@ __device__ __forceinline__ void panel_load(double *S, int kp, const double *X, i
   }
 }
 
+// ---- look-ahead downdate helpers (row-cyclic tile ownership) ------------
+// A warp owns row groups gg = tw + i*TW (slot i).  The active slots of a
+// column step are always a suffix [i0, MAXT); they are processed by fully
+// unrolled, branch-free slot loops (rows past gm are clamped to a valid row
+// and their results discarded), so every DMMA issues from converged code.
+
+template <int MAXT, int TW>
+__device__ __forceinline__ int first_slot(int tw, int lo) {
+  const int d = lo - tw;
+  return d <= 0 ? 0 : (d + TW - 1) / TW;
+}
+
+// a[i] = C(gg_i, cb) [+ A_gg B_cb^T] - sum_{k < kend blocks} L(gg_i, k) L(cb, k)^T for i >= I0
+template <int MAXT, int TW, int I0, bool SK>
+__device__ __forceinline__ void dd_suffix(double (&a)[MAXT][2], const double *S, const Tri &t, const double *SA,
+                                          const double *SB, int kp, int tw, int gm, int cb, int kend, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  int fa[MAXT];
+#pragma unroll
+  for (int i = I0; i < MAXT; ++i) {
+    const int gg = min(tw + i * TW, gm - 1);
+    a[i][0] = S[t.off(8 * gg + fr, 8 * cb + 2 * fc)];
+    a[i][1] = S[t.off(8 * gg + fr, 8 * cb + 2 * fc + 1)];
+    fa[i] = tri_frag(t, gg, 0, lane);
+  }
+  if (SK) {
+    const int po = (lane >> 4) * 4 * kp + 4 * fc + (fr & 3);
+    const int pb = 2 * cb * 4 * kp + po;
+    for (int kk = 0; kk < kp / 4; ++kk) {
+      const double bv = SB[pb + 16 * kk];
+#pragma unroll
+      for (int i = I0; i < MAXT; ++i) {
+        const int gg = min(tw + i * TW, gm - 1);
+        dmma(a[i], SA[2 * gg * 4 * kp + po + 16 * kk], bv);
+      }
+    }
+  }
+  const int fb = tri_frag(t, cb, 0, lane);
+#pragma unroll 2
+  for (int kk = 0; kk < 2 * kend; ++kk) {
+    const double bv = S[fb + 16 * kk];
+#pragma unroll
+    for (int i = I0; i < MAXT; ++i) dmma(a[i], -S[fa[i] + 16 * kk], bv);
+  }
+}
+
+template <int MAXT, int TW, bool SK>
+__device__ __forceinline__ void downdate_tiles(double (&a)[MAXT][2], const double *S, const Tri &t, const double *SA,
+                                               const double *SB, int kp, int tw, int gm, int lo, int cb, int kend,
+                                               int lane) {
+  const int i0 = first_slot<MAXT, TW>(tw, lo);
+#define PB_DD(I_) \
+  if (MAXT > I_ && i0 == I_) dd_suffix<MAXT, TW, (MAXT > I_ ? I_ : 0), SK>(a, S, t, SA, SB, kp, tw, gm, cb, kend, lane);
+  PB_DD(0) PB_DD(1) PB_DD(2) PB_DD(3) PB_DD(4) PB_DD(5) PB_DD(6) PB_DD(7)
+#undef PB_DD
+}
+
+// a[i] = p[i] - L(gg_i, kb) L(cb, kb)^T for i >= I0 (one column block)
+template <int MAXT, int TW, int I0>
+__device__ __forceinline__ void ab_suffix(double (&a)[MAXT][2], const double (&p)[MAXT][2], const double *S,
+                                          const Tri &t, int tw, int gm, int cb, int kb, int lane) {
+  const int fb = tri_frag(t, cb, 0, lane) + 32 * kb;
+  const double b0 = S[fb], b1 = S[fb + 16];
+#pragma unroll
+  for (int i = I0; i < MAXT; ++i) {
+    const int gg = min(tw + i * TW, gm - 1);
+    const int fa = tri_frag(t, gg, 0, lane) + 32 * kb;
+    a[i][0] = p[i][0], a[i][1] = p[i][1];
+    dmma(a[i], -S[fa], b0);
+    dmma(a[i], -S[fa + 16], b1);
+  }
+}
+
+template <int MAXT, int TW>
+__device__ __forceinline__ void add_block_tiles(double (&a)[MAXT][2], const double (&p)[MAXT][2], const double *S,
+                                                const Tri &t, int tw, int gm, int lo, int cb, int kb, int lane) {
+  const int i0 = first_slot<MAXT, TW>(tw, lo);
+#define PB_AB(I_) \
+  if (MAXT > I_ && i0 == I_) ab_suffix<MAXT, TW, (MAXT > I_ ? I_ : 0)>(a, p, S, t, tw, gm, cb, kb, lane);
+  PB_AB(0) PB_AB(1) PB_AB(2) PB_AB(3) PB_AB(4) PB_AB(5) PB_AB(6) PB_AB(7)
+#undef PB_AB
+}
+
 // GM/GN > 0 fix the row/column group counts at compile time (the common
 // square sizes): every tile loop then unrolls and all tri-layout offsets
 // fold to constants; GM = GN = 0 is the generic runtime-shaped kernel.
 // SK: fused syrk_potrf -- the item's A (and B) windows sit next to the tri
 // buffer and every tile's downdate also accumulates + A_g B_j^T, exactly
 // the per-tile order of syrk_potrf_drv (ccore.pyx:908-941).
-template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false>
-__global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
   extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int team = warp / TW, tw = warp % TW;
@@ -101,6 +217,7 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   double *dinv = S0 + (DB ? 2 : 1) * tri_elems;         // cn8 doubles
   volatile int *flag = (volatile int *)(dinv + t.cn8);  // failure index
   double *Wp = dinv + t.cn8 + 8;                        // inverted diagonal block (64)
+  uint64_t *tbar = reinterpret_cast<uint64_t *>(dinv + t.cn8 + 1);  // bulk-load barrier
   // SK operands: A rows padded to 8*gm, B rows to 8*gn, panel length kp
   const int kp = SK ? (int)((g.k + 3) & ~(ix)3) : 0;
   double *SA = Wp + 64;
@@ -109,6 +226,21 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
   const bool aligned_out = (g.di & 3) == 0;
   const bool vin = vec_in != 0;
   const ix stride = (ix)gridDim.x * teams_per_cta;
+  // bulk (TMA) tri staging and write-back: single-buffered, aligned items
+  const bool bulk_in = !DB && vin;
+  const bool bulk_out = !DB && vec_out != 0;
+  unsigned phase = 0;
+  if (bulk_in) {
+    if (ttid == 0) {
+      mbar_init(tbar, 1);
+      mbar_fence_init();
+    }
+    team_sync(bar, tthreads);
+  }
+  auto load_item = [&](ix bb) {
+    if (bulk_in) tri_load_bulk(S0, t, g.C.item(bb), g.C.cn, g.ci, g.cj, m, n, gm, tbar, ttid, tthreads);
+    else tri_load(S0, t, g.C.item(bb), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+  };
 
   auto skip = [&](ix b) { return g.merge && g.info[b] >= 0; };
   ix b = (ix)blockIdx.x * teams_per_cta + team;
@@ -120,7 +252,7 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     }
   };
   if (b < g.batch) {
-    tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+    load_item(b);
     stage_ab(b);
   }
   cp_async_commit();
@@ -135,72 +267,102 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
+      if (bulk_in) {
+        mbar_wait(tbar, phase);
+        phase ^= 1;
+      }
     }
     if (ttid == 0) *flag = -1;
     team_sync(bar, tthreads);
 
     int fail = -1;
+    // Look-ahead left-looking schedule.  Tile rows are owned row-cyclically
+    // (row group gg by warp gg % TW, slot i = gg / TW), so the diagonal
+    // tile of column block jb belongs to warp jb % TW.  While that warp runs
+    // the serial 8x8 factor + inverse, every other warp completes its
+    // column-jb tiles and already accumulates the downdate of column block
+    // jb+1 over blocks 0..jb-1 (acc_nx); the next step then adds only block
+    // jb's contribution (two DMMAs) before factoring.
+    double acc_nx[MAXT][2];
+    bool prep = false;  // acc_nx holds column block jb's partial (blocks < jb-1 applied)
+#pragma unroll
+    for (int i = 0; i < MAXT; ++i) acc_nx[i][0] = acc_nx[i][1] = 0.0;
 #pragma unroll(GN > 0 ? GN : 1)
     for (int jb = 0; jb < (GN > 0 ? GN : 64); ++jb) {
       if (GN == 0 && jb >= t.gn) break;
       const int ncol = min(8, n - 8 * jb);
+      const bool is_d = TW == 1 || tw == jb % TW;
       double acc[MAXT][2];
-      // downdate every row-group tile of this column block this warp owns
+      if (is_d) {
+        // ---- diagonal warp: complete the diagonal tile, factor, invert
+        const int id = jb / TW;  // slot of row group jb
+        double dg[2];
+        if (prep) {
+          const int fb = tri_frag(t, jb, 0, lane) + 32 * (jb - 1);
+          dg[0] = dg[1] = 0.0;
 #pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int gg = jb + tw + u * TW;
-        if (gg < gm) {
-          acc[u][0] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc)];
-          acc[u][1] = S[t.off(8 * gg + fr, 8 * jb + 2 * fc + 1)];
+          for (int i = 0; i < MAXT; ++i)
+            if (i == id) dg[0] = acc_nx[i][0], dg[1] = acc_nx[i][1];  // static register indexing
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) dmma(dg, -S[fb + 16 * kk], S[fb + 16 * kk]);
+        } else {
+          dg[0] = S[t.off(8 * jb + fr, 8 * jb + 2 * fc)];
+          dg[1] = S[t.off(8 * jb + fr, 8 * jb + 2 * fc + 1)];
           if (SK) {
-            const int pa = (2 * gg + (lane >> 4)) * 4 * kp + 4 * fc + (fr & 3);
             const int pb = (2 * jb + (lane >> 4)) * 4 * kp + 4 * fc + (fr & 3);
 #pragma unroll 4
-            for (int kk = 0; kk < kp / 4; ++kk) dmma(acc[u], SA[pa + 16 * kk], SB[pb + 16 * kk]);
+            for (int kk = 0; kk < kp / 4; ++kk) dmma(dg, SA[pb + 16 * kk], SB[pb + 16 * kk]);
           }
-          const int fa = tri_frag(t, gg, 0, lane), fb = tri_frag(t, jb, 0, lane);
+          const int fb = tri_frag(t, jb, 0, lane);
 #pragma unroll 4
-          for (int kk = 0; kk < 2 * jb; ++kk) dmma(acc[u], -S[fa + 16 * kk], S[fb + 16 * kk]);
+          for (int kk = 0; kk < 2 * jb; ++kk) dmma(dg, -S[fb + 16 * kk], S[fb + 16 * kk]);
         }
-      }
-      // diagonal tile (owned by tw == 0, u == 0): factor, then its inverse;
-      // the other tiles park their downdated values in shared memory
-      if (tw == 0) {
-        const int f = factor_diag_tile(acc[0], ncol, dinv + 8 * jb, lane);
+        double wi[2];
+        const int f = factor_inv_tile(dg, wi, ncol, dinv + 8 * jb, lane);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * fc + e;
-          if (c < ncol && (f < 0 || c < f)) S[t.off(8 * jb + fr, 8 * jb + c)] = acc[0][e];
+          if (c < ncol && (f < 0 || c < f)) S[t.off(8 * jb + fr, 8 * jb + c)] = dg[e];
         }
         if (f >= 0 && lane == 0) *flag = 8 * jb + f;
-        __syncwarp();
-        if (f < 0 && jb + 1 < gm) build_inv_block(S, t, jb, dinv, ncol, Wp, lane);
+        if (f < 0 && jb + 1 < gm) store_inv_block(wi, Wp, lane);
+        // then this warp's other column-jb tiles
+        if (prep) add_block_tiles<MAXT, TW>(acc, acc_nx, S, t, tw, gm, jb + 1, jb, jb - 1, lane);
+        else downdate_tiles<MAXT, TW, SK>(acc, S, t, SA, SB, kp, tw, gm, jb + 1, jb, jb, lane);
+      } else {
+        // ---- other warps: column-jb tiles now, column-(jb+1) partials next
+        if (prep) add_block_tiles<MAXT, TW>(acc, acc_nx, S, t, tw, gm, jb + 1, jb, jb - 1, lane);
+        else downdate_tiles<MAXT, TW, SK>(acc, S, t, SA, SB, kp, tw, gm, jb + 1, jb, jb, lane);
       }
+      // park the column-jb tiles below the diagonal (A operand of the solve)
 #pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int gg = jb + tw + u * TW;
-        if (gg < gm && gg > jb) {
+      for (int i = 0; i < MAXT; ++i) {
+        const int gg = tw + i * TW;
+        if (gg > jb && gg < gm) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) S[t.off(8 * gg + fr, 8 * jb + 2 * fc + e)] = acc[u][e];
+          for (int e = 0; e < 2; ++e) S[t.off(8 * gg + fr, 8 * jb + 2 * fc + e)] = acc[i][e];
         }
       }
+      const bool look = TW > 1 && !is_d && jb + 1 < t.gn;
+      if (look) downdate_tiles<MAXT, TW, SK>(acc_nx, S, t, SA, SB, kp, tw, gm, jb + 1, jb + 1, jb, lane);
       team_sync(bar, tthreads);
       fail = *flag;
       if (fail >= 0) break;
       // solve the tiles below the diagonal: X := X * L_jj^{-T} on DMMA
 #pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int gg = jb + tw + u * TW;
-        if (gg < gm && gg > jb) {
-          apply_inv_block(acc[u], S, t, gg, jb, Wp, lane);
+      for (int i = 0; i < MAXT; ++i) {
+        const int gg = tw + i * TW;
+        if (gg > jb && gg < gm) {
+          apply_inv_block(acc[i], S, t, gg, jb, Wp, lane);
           __syncwarp();
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 2 * fc + e;
-            if (c < ncol) S[t.off(8 * gg + fr, 8 * jb + c)] = acc[u][e];
+            if (c < ncol) S[t.off(8 * gg + fr, 8 * jb + c)] = acc[i][e];
           }
         }
       }
+      prep = look;
       team_sync(bar, tthreads);
     }
 
@@ -208,7 +370,32 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     // reference's block-row order would have stored, ccore.pyx:884-899)
     double *D = g.D.item(b);
     const int iif = fail >= 0 ? (fail & ~3) : 0;
-    if (fail < 0 || aligned_out) {
+    if (fail < 0 && bulk_out) {
+      // whole 4-row panels strictly below the diagonal: one bulk store
+      // each (thread 0); the 4x4 diagonal pieces and a partial last panel
+      // element-wise.  The loop's last team_sync ordered every thread's
+      // shared stores; the fence hands them to the async proxy.
+      fence_proxy_async();
+      team_sync(bar, tthreads);
+      for (int gg = 0; gg < gm; ++gg) {
+        const int w = t.width(gg), base = t.group_off(gg);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r0 = 8 * gg + 4 * h;
+          if (r0 >= m) continue;
+          const double *src = S + base + h * 4 * w;
+          const bool full = r0 + 4 <= m;
+          const int cl = full ? min(r0, n) : 0;
+          if (cl > 0 && ttid == 0) tma_store_1d(D + eo(g.di + r0, g.dj, g.D.cn), src, 32u * (unsigned)cl);
+          const int ce = min(r0 + 4, n);
+          for (int q = ttid; q < 4 * (ce - cl); q += tthreads) {
+            const int c = cl + (q >> 2), r = r0 + (q & 3);
+            if (r < m && c <= r) D[eo(g.di + r, g.dj + c, g.D.cn)] = src[4 * c + (q & 3)];
+          }
+        }
+      }
+      if (ttid == 0) bulk_commit();
+    } else if (fail < 0 || aligned_out) {
       for (int gg = 0; gg < gm; ++gg) {
         const int w = t.width(gg), base = t.group_off(gg);
 #pragma unroll
@@ -244,16 +431,18 @@ __global__ void __launch_bounds__(256) potrf_team_kernel(PotrfArgs g, int team_e
     const int nd = fail >= 0 ? fail : n;
     for (int c = ttid; c < nd; c += tthreads) dA[g.dj + c] = dinv[c];
     if (ttid == 0 && g.info) g.info[b] = fail >= 0 ? fail + g.info_offset : -1;
+    if (bulk_out && ttid == 0) bulk_wait_read0();  // S is free once the stores have read it
     team_sync(bar, tthreads);
     b = nb;
     if (DB && vin) cur ^= 1;
     else if (b < g.batch) {
-      tri_load(S0, t, g.C.item(b), g.C.cn, g.ci, g.cj, m, n, gm, vin, ttid, tthreads);
+      load_item(b);
       stage_ab(b);
       cp_async_commit();
     }
   }
   cp_async_wait<0>();
+  if (bulk_out && ttid == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -361,9 +550,9 @@ static ix syrk_operand_elems(ix m, ix n, ix k, bool ab_same) {
   return (m + 7) / 8 * 8 * kp + (ab_same ? 0 : (n + 7) / 8 * 8 * kp);
 }
 
-template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false>
+template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false, int MINB = 1>
 static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
-  auto kern = potrf_team_kernel<TW, MAXT, DB, GM, GN, SK>;
+  auto kern = potrf_team_kernel<TW, MAXT, DB, GM, GN, SK, MINB>;
   const ix cn8 = (g.n + 7) / 8 * 8;
   ix team_elems = Tri::size(g.m, g.n) * (DB ? 2 : 1) + cn8 + 8 + 64 +
                   (SK ? syrk_operand_elems(g.m, g.n, g.k, g.ab_same != 0) : 0);
@@ -401,13 +590,13 @@ cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   // compile-time shaped instances for the common (benchmark) sizes
   // measured on B200 (profiles/r01_potrf_team_tuning.txt): more, smaller
   // teams without double buffering win where the diagonal chain dominates
-  if (gm == 4 && gn == 4) return launch_potrf<1, 4, false, 4, 4>(g, st);
-  if (gm == 8 && gn == 8) return launch_potrf<2, 4, false, 8, 8>(g, st);
-  if (gm <= 2) return db ? launch_potrf<1, 2, true>(g, st) : launch_potrf<1, 2, false>(g, st);
-  if (gm <= 4) return db ? launch_potrf<1, 4, true>(g, st) : launch_potrf<1, 4, false>(g, st);
-  if (gm <= 8) return db ? launch_potrf<4, 2, true>(g, st) : launch_potrf<4, 2, false>(g, st);
-  if (gm <= 16) return launch_potrf<8, 2, false>(g, st);
-  if (gm <= 32) return launch_potrf<8, 4, false>(g, st);
+  if (gm == 4 && gn == 4) return launch_potrf<1, 4, false, 4, 4, false, 4>(g, st);
+  if (gm == 8 && gn == 8) return launch_potrf<2, 4, false, 8, 8, false, 3>(g, st);
+  if (gm <= 2) return db ? launch_potrf<1, 2, true, 0, 0, false, 4>(g, st) : launch_potrf<1, 2, false, 0, 0, false, 4>(g, st);
+  if (gm <= 4) return db ? launch_potrf<1, 4, true, 0, 0, false, 4>(g, st) : launch_potrf<1, 4, false, 0, 0, false, 4>(g, st);
+  if (gm <= 8) return db ? launch_potrf<4, 2, true, 0, 0, false, 3>(g, st) : launch_potrf<4, 2, false, 0, 0, false, 3>(g, st);
+  if (gm <= 16) return launch_potrf<8, 2, false, 0, 0, false, 3>(g, st);
+  if (gm <= 32) return launch_potrf<8, 4, false, 0, 0, false, 2>(g, st);
   return launch_potrf<8, 8, false>(g, st);
 }
 
@@ -420,11 +609,11 @@ bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same) {
 // fused syrk + potrf: single-buffered generic team shapes
 cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st) {
   const ix gm = (g.m + 7) / 8;
-  if (gm <= 2) return launch_potrf<1, 2, false, 0, 0, true>(g, st);
-  if (gm <= 4) return launch_potrf<1, 4, false, 0, 0, true>(g, st);
-  if (gm <= 8) return launch_potrf<4, 2, false, 0, 0, true>(g, st);
-  if (gm <= 16) return launch_potrf<8, 2, false, 0, 0, true>(g, st);
-  if (gm <= 32) return launch_potrf<8, 4, false, 0, 0, true>(g, st);
+  if (gm <= 2) return launch_potrf<1, 2, false, 0, 0, true, 4>(g, st);
+  if (gm <= 4) return launch_potrf<1, 4, false, 0, 0, true, 4>(g, st);
+  if (gm <= 8) return launch_potrf<4, 2, false, 0, 0, true, 3>(g, st);
+  if (gm <= 16) return launch_potrf<8, 2, false, 0, 0, true, 3>(g, st);
+  if (gm <= 32) return launch_potrf<8, 4, false, 0, 0, true, 2>(g, st);
   return launch_potrf<8, 8, false, 0, 0, true>(g, st);
 }
 

@@ -88,6 +88,65 @@ __device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double
 }
 
 
+// Cholesky factor AND inverse of the 8x8 diagonal tile in one column sweep
+// (fragment layout: lane holds row lane>>2, cols 2(lane&3)+e).  Column c:
+// one shuffle for the pivot, rsqrt, scale, three shuffles for the rank-1
+// update of the trailing tile; the inverse W = L^{-1} is forward-substituted
+// in the same sweep (row c of W scaled by 1/L[c,c], rows below updated),
+// so its chain overlaps the factor's.  Returns the first failing column or
+// -1; dinv_out[c] = 1/L[c,c]; W's rows/cols past ncol are unused.
+// 1/sqrt(d) to ~1 ulp: MUFU seed + two Newton steps, branch-free (the
+// library rsqrt() carries special-case paths that break warp convergence).
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+__device__ __forceinline__ int factor_inv_tile(double (&x)[2], double (&w)[2], int ncol, double *dinv_out, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  int fail = -1;
+  w[0] = (fr == 2 * fc) ? 1.0 : 0.0;
+  w[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
+  // Branch-free sweep (every lane runs every column; the pivot test only
+  // records the first failure -- values past it are never stored).
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double d = __shfl_sync(0xffffffffu, x[c & 1], c * 4 + (c >> 1));
+    const bool live = c < ncol && fail < 0;
+    if (live && d <= 0.0) fail = c;  // NaN passes, as in the reference (ccore.pyx:423)
+    const double inv = rsqrt_nr(d);
+    const bool own = fc == (c >> 1);
+    const double xs = x[c & 1];
+    x[c & 1] = own && fr == c ? d * inv : (own && fr > c ? __dmul_rn(xs, inv) : xs);
+    if (fr == c) {
+      w[0] = __dmul_rn(w[0], inv);
+      w[1] = __dmul_rn(w[1], inv);
+    }
+    if (lane == 0 && live && fail < 0) dinv_out[c] = inv;
+    const double lrc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
+    const double l0 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc) * 4 + (c >> 1));
+    const double l1 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc + 1) * 4 + (c >> 1));
+    const double wc0 = __shfl_sync(0xffffffffu, w[0], c * 4 + fc);
+    const double wc1 = __shfl_sync(0xffffffffu, w[1], c * 4 + fc);
+    x[0] = 2 * fc > c ? fma(-lrc, l0, x[0]) : x[0];
+    x[1] = 2 * fc + 1 > c ? fma(-lrc, l1, x[1]) : x[1];
+    w[0] = fr > c ? fma(-lrc, wc0, w[0]) : w[0];
+    w[1] = fr > c ? fma(-lrc, wc1, w[1]) : w[1];
+  }
+  return fail;
+}
+
+// Store W (from factor_inv_tile) as the B operand of apply_inv_block.
+__device__ __forceinline__ void store_inv_block(const double (&w)[2], double *Wp, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) Wp[(fr >> 2) * 32 + 4 * (2 * fc + e) + (fr & 3)] = w[e];
+}
+
 // W = L_jj^{-1} of the 8x8 diagonal block (rows/cols 8j..), written to Wp in
 // panel layout (element (n, k) at (n>>2)*32 + 4k + (n&3)) so that it is read
 // back as the B operand of an m8n8k4 MMA:  X * L_jj^{-T} = X * W^T.  Built by

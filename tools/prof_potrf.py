@@ -7,6 +7,8 @@ from paper_1704_02457_b200 import level3, pack
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, (1 << 31) // (n * n * 8 * 4))
+if nb == 0:  # C2 batch: ~2^34 flop, capped at the bench's resident chunk
+    nb = min(round(2 ** 34 / (n ** 3 / 3.0)), int(6e9 // (2 * 8 * (n + 4) * (n + 4))))
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 g = torch.Generator(device="cuda").manual_seed(0)
 M = torch.rand((nb, n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
