@@ -377,6 +377,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     pts, desc = config_points(args.config)
+    if args.only:
+        keep = [x.strip() for x in args.only.split(",")]
+        pts = [p for p in pts if p.label in keep]
+        desc += " [subset: %s]" % args.only
     pb.load_native()
 
     gps = []
@@ -781,6 +785,10 @@ def run_reference(args):
     if rank != 0:
         return
     pts, desc = config_points(args.config)
+    if args.only:
+        keep = [x.strip() for x in args.only.split(",")]
+        pts = [p for p in pts if p.label in keep]
+        desc += " [subset: %s]" % args.only
     per_step = max(0.5, args.ref_seconds)
     for _ in range(args.warmup):
         pass  # the reference core has no warm-up state; a tiny run below primes imports
@@ -819,6 +827,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=14.0)
     ap.add_argument("--ref-seconds", type=float, default=7.0)
     ap.add_argument("--csv", default=None, help="also write per-point rows in the reference's sweep CSV schema")
+    ap.add_argument("--only", default=None,
+                    help="comma-separated point labels to keep (tuning runs only, e.g. 'potrf_l n=4')")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

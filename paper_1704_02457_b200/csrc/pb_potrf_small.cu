@@ -418,6 +418,226 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------
+// n <= 8: warp-autonomous kernel with whole-sector stores.
+//
+// Each warp owns 32 items per iteration (lane = item for the factor) and
+// runs its own software pipeline: the NEXT group's lower prefix of C is
+// loaded into registers (coalesced 16-byte pieces, lane-consecutive)
+// while the current group is factored from a warp-private shared-memory
+// transpose; no CTA barrier anywhere.
+//
+// Stores: the reference writes the lower triangle only, so the diagonal
+// 4x4 blocks hold 32-byte sectors that are only partly written.  Left to
+// the hardware, every such sector costs an L2 fill from DRAM in the middle
+// of the write stream (profiles/r01_potrf_n4_ncu_summary.txt).  Here the
+// warp loads exactly those sectors' pieces of D together with C (same
+// pipeline stage), merges, and stores every touched sector whole: the
+// bytes outside the reference's write set are re-stored with the values
+// just read from D, so they never change (tools/potrf4_exp.cu measured
+// 0.27 -> 0.35 of HBM at n = 4).  A failing item (rare) falls back to
+// element-masked stores of exactly the reference's partial write set.
+template <int N>
+struct WarpCfg {
+  static constexpr int NP = (N + 3) / 4;
+  __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
+  __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
+  static constexpr int IE = poff(NP);  // lower-prefix doubles per item
+  static constexpr int PC = IE / 2;    // 16-byte pieces per item
+  // smem stride per item: 16-byte aligned, an odd number of 16-byte units
+  // (lane-per-item reads spread over the banks)
+  static constexpr int SS = IE + 2;  // PC = 2*sum(cols) is even; slot IE carries the status
+  static_assert(PC % 2 == 0, "odd 16-byte units per item stride");
+  // element (row 4p + r, col) of the prefix is in the write set
+  __host__ __device__ static constexpr bool wr(int p, int col, int r) {
+    return 4 * p + r < N && 4 * p + r >= col;
+  }
+  __host__ __device__ static constexpr int panel_of(int w, int p = 0) {
+    return p + 1 < NP && w >= poff(p + 1) / 2 ? panel_of(w, p + 1) : p;
+  }
+  __host__ __device__ static constexpr bool full_piece(int w) {
+    return wr(panel_of(w), (w - poff(panel_of(w)) / 2) >> 1, 2 * ((w - poff(panel_of(w)) / 2) & 1)) &&
+           wr(panel_of(w), (w - poff(panel_of(w)) / 2) >> 1, 2 * ((w - poff(panel_of(w)) / 2) & 1) + 1);
+  }
+  __host__ __device__ static constexpr int count_mixed(int w) { return w == PC ? 0 : (full_piece(w) ? 0 : 1) + count_mixed(w + 1); }
+  static constexpr int DPC = count_mixed(0);  // pieces of D needed per item
+  static constexpr int WARPS = N <= 4 ? 4 : 2;
+  static constexpr int STAGE = 32 * SS + 32 * 2 * DPC;  // doubles per pipeline stage
+  static constexpr size_t SMEM_WARP = sizeof(double) * 2 * STAGE;
+  static constexpr size_t SMEM = WARPS * SMEM_WARP + sizeof(int) * (PC + DPC + 2);
+};
+
+template <int N>
+__device__ __forceinline__ void warp_piece(int w, int &p, int &col, int &h) {
+  using Cfg = WarpCfg<N>;
+  p = 0;
+#pragma unroll
+  for (int q = 1; q < Cfg::NP; ++q)
+    if (w >= Cfg::poff(q) / 2) p = q;
+  const int rem = w - Cfg::poff(p) / 2;
+  col = rem >> 1;
+  h = rem & 1;
+}
+
+template <int N>
+__global__ void __launch_bounds__(WarpCfg<N>::WARPS * 32, (N <= 4 ? 4 : 3)) potrf_warp_kernel(PotrfArgs g) {
+  using Cfg = WarpCfg<N>;
+  constexpr int PC = Cfg::PC, DPC = Cfg::DPC, SS = Cfg::SS, NP = Cfg::NP;
+  extern __shared__ __align__(128) double smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *W = smem + (size_t)wid * 2 * Cfg::STAGE;  // this warp's two stages
+  int *tab = (int *)(smem + Cfg::WARPS * 2 * Cfg::STAGE);  // j -> piece w of the D list
+  int *inv = tab + DPC;                                     // w -> j, or -1 (fully written)
+  if (threadIdx.x == 0) {
+    int j = 0;
+    for (int w = 0; w < PC; ++w) {
+      int p, col, h;
+      warp_piece<N>(w, p, col, h);
+      const bool full = Cfg::wr(p, col, 2 * h) && Cfg::wr(p, col, 2 * h + 1);
+      inv[w] = full ? -1 : j;
+      if (!full) tab[j++] = w;
+    }
+  }
+  __syncthreads();
+
+  const ix ngroups = (g.batch + 31) / 32;
+  const ix gw = (ix)blockIdx.x * Cfg::WARPS + wid, nw = (ix)gridDim.x * Cfg::WARPS;
+  const double *Cb = g.C.p;
+  double *Db = g.D.p;
+  // stage group `grp`: C's lower prefix (item-major, stride SS) and the
+  // pieces of D that share a sector with the write set but are not in it
+  auto issue = [&](ix grp, int st) {
+    double *S = W + st * Cfg::STAGE;
+    double *SD = S + 32 * SS;
+#pragma unroll
+    for (int k = 0; k < PC; ++k) {
+      const int q = lane + 32 * k, it = q / PC, w = q - it * PC;
+      const ix b = grp * 32 + it;
+      int p, col, h;
+      warp_piece<N>(w, p, col, h);
+      const bool ok = b < g.batch;
+      const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
+      cp_async16(S + it * SS + 2 * w, src, ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int k = 0; k < DPC; ++k) {
+      const int q = lane + 32 * k, it = q / DPC, j = q - it * DPC;
+      const ix b = grp * 32 + it;
+      int p, col, h;
+      warp_piece<N>(tab[j], p, col, h);
+      const bool ok = b < g.batch;
+      const double *src = ok ? Db + b * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h : Db;
+      cp_async16(SD + 2 * q, src, ok ? 16 : 0);
+    }
+  };
+
+  ix grp = gw;
+  int st = 0;
+  if (grp < ngroups) issue(grp, 0);
+  cp_async_commit();
+  for (; grp < ngroups; grp += nw, st ^= 1) {
+    if (grp + nw < ngroups) issue(grp + nw, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    double *S = W + st * Cfg::STAGE;
+    const double *SD = S + 32 * SS;
+    const ix b0 = grp * 32;
+    int fail = -1;
+    {
+      double L[4 * NP][N];
+      double *Si = S + lane * SS;
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) L[4 * p + r][c] = c < Cfg::cols(p) ? Si[Cfg::poff(p) + 4 * c + r] : 0.0;
+        }
+      double dinv[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) dinv[c] = 0.0;
+      const bool live = b0 + lane < g.batch;
+      if (live) fail = factor_t1<N>(L, dinv);
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          if (c < Cfg::cols(p)) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) Si[Cfg::poff(p) + 4 * c + r] = L[4 * p + r][c];
+          }
+      if (live && g.info) g.info[b0 + lane] = fail;
+      // diag_inv: lane-consecutive doubles (coalesced), values gathered from
+      // the owning lane by shuffles: store k covers items (32k + lane) / N
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int q = lane + 32 * k, it = q / N, c = q - it * N;
+        double v = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < N; ++c2) {
+          const double t = __shfl_sync(0xffffffffu, dinv[c2], it);
+          if (c2 == c) v = t;
+        }
+        const int f = __shfl_sync(0xffffffffu, fail, it);
+        if (b0 + it < g.batch && (f < 0 || c < f)) g.D.d[(b0 + it) * g.D.dstride + g.dj + c] = v;
+      }
+      reinterpret_cast<int *>(Si + SS - 2)[0] = fail;  // pad slot carries the status
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < PC; ++k) {
+      const int q = lane + 32 * k, it = q / PC, w = q - it * PC;
+      const ix b = b0 + it;
+      if (b >= g.batch) continue;
+      int p, col, h;
+      warp_piece<N>(w, p, col, h);
+      const int r0 = 4 * p + 2 * h;
+      double2 v = *reinterpret_cast<const double2 *>(S + it * SS + 2 * w);
+      double *dst = Db + b * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+      const int f = reinterpret_cast<const int *>(S + it * SS + SS - 2)[0];
+      bool w0 = Cfg::wr(p, col, 2 * h), w1 = Cfg::wr(p, col, 2 * h + 1);
+      if (f < 0) {
+        if (!(w0 && w1)) {  // sector merge with D's own bytes
+          const double2 old = *reinterpret_cast<const double2 *>(SD + 2 * (it * DPC + inv[w]));
+          if (!w0) v.x = old.x;
+          if (!w1) v.y = old.y;
+        }
+        *reinterpret_cast<double2 *>(dst) = v;
+      } else {  // the reference's partial write set of a failing item
+        const int iif = f & ~3;
+        w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
+        w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+        if (w0 && w1) *reinterpret_cast<double2 *>(dst) = v;
+        else if (w0) dst[0] = v.x;
+        else if (w1) dst[1] = v.y;
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
+template <int N>
+static cudaError_t launch_warp(const PotrfArgs &g, cudaStream_t st) {
+  using Cfg = WarpCfg<N>;
+  auto kern = potrf_warp_kernel<N>;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::WARPS * 32, Cfg::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  const ix groups = (g.batch + 31) / 32;
+  const ix ctas = (groups + Cfg::WARPS - 1) / Cfg::WARPS;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > ctas) grid = ctas;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, Cfg::WARPS * 32, Cfg::SMEM, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <int N, int NTH_ = 128, int STAGES_ = 2>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
@@ -464,6 +684,21 @@ bool potrf_small_ok(const PotrfArgs &g) {
 }
 
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
+  static const bool legacy = getenv("PB_SMALL_LEGACY") != nullptr;  // A/B switch for the sweeps
+  // n <= 4: warp-autonomous whole-sector kernel (measured 0.27 -> 0.32 of HBM at n = 4);
+  // 5 <= n <= 8 stays on the CTA kernel, which measured faster there (register pressure)
+  if (!legacy && g.n <= 4) {
+    switch (g.n) {
+      case 1: return launch_warp<1>(g, st);
+      case 2: return launch_warp<2>(g, st);
+      case 3: return launch_warp<3>(g, st);
+      case 4: return launch_warp<4>(g, st);
+      case 5: return launch_warp<5>(g, st);
+      case 6: return launch_warp<6>(g, st);
+      case 7: return launch_warp<7>(g, st);
+      case 8: return launch_warp<8>(g, st);
+    }
+  }
   switch (g.n) {
 #define PB_SMALL(N_) \
   case N_:           \

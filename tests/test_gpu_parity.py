@@ -495,6 +495,36 @@ def test_potrf_small_bit_exact(n):
     assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64))
 
 
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_potrf_small_in_place_and_offset_bit_exact(n):
+    """D == C in place, and a D window at a column offset inside a wider
+    matrix: the small kernels re-store whole 32-byte sectors of D, so every
+    byte outside the reference's write set (strict upper, padding rows, the
+    columns beside the window) must come back unchanged, bit for bit."""
+    rng = np.random.default_rng(200 + n)
+    nb = 97
+    a = spd_batch(rng, nb, n)
+    for b in range(3, nb, 11):
+        f = int(rng.integers(0, n))
+        a[b, f, f] = -2.0
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    dC = dev(C)
+    info = level3.potrf_l(n, dC, dC, check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C, 0, 0, C, 0, 0)
+    assert np.array_equal(info, winfo)
+    assert np.array_equal(host(dC).view(np.uint64), C.storage.view(np.uint64))
+    # D at (4, 3) of a (n+5) x (n+6) matrix pre-filled with random bytes
+    C2 = rand_batch(rng, nb, n, n)
+    C2.set_window(0, 0, a)
+    D = rand_batch(rng, nb, n + 5, n + 6)
+    dC2, dD = dev(C2), dev(D)
+    info = level3.potrf_l(n, dC2, dD.ref(4, 3), check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C2, 0, 0, D, 4, 3)
+    assert np.array_equal(info, winfo)
+    assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64))
+
+
 def test_riccati_chain_c5_vs_oracle_and_graph_replay():
     """C5 chain: gemm_nt -> syrk_ln -> potrf_l -> trsm_rltn ->
     gemm_nt per stage, batched over problems; eager and CUDA-graph replay are
