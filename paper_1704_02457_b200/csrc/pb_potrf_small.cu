@@ -9,7 +9,8 @@
 //    triangle, columns [0, 4p+4), is a contiguous run in panel-major);
 //  * every lane of a warp issues consecutive 16-byte pieces, so loads and
 //    the masked stores of the results are fully coalesced;
-//  * n <= 8: one thread owns one item, entirely in registers;
+//  * n <= 8: one thread owns one item, entirely in registers, and every
+//    touched 32-byte sector of D is stored whole (potrf_small1_kernel);
 //    9 <= n <= 16: a quad of threads owns one item, thread q owning panel q
 //    (rows 4q..4q+3), left-looking over 4-column blocks, computed in place
 //    in the staged shared-memory copy (block rows read back by broadcast).
@@ -236,7 +237,7 @@ __device__ __forceinline__ int factor_t4s(double *Si, double *dinv, int q, volat
   return fail;
 }
 
-template <int N, int NTH_, int STAGES_>
+template <int N, int NTH_, int STAGES_, bool QRMW = false>
 __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
   constexpr int STG = Cfg::STAGES;
@@ -281,20 +282,50 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
     if (r0 < nrounds) issue(r0, s0);
     cp_async_commit();
   }
+  // Whole-sector stores for the quad path (T == 4, two stages): the strict
+  // upper of the diagonal blocks is only ever READ by factor_t4s (into
+  // discarded accumulator entries), so D's bytes for those elements are
+  // cp.async'd into their own slots while the factor runs; full panels then
+  // store every piece whole (no L2 fills from DRAM mid write stream).
+  // Panels with padding rows (n % 4 != 0) keep element-masked stores.
+  // Opt-in (PB_QUAD_RMW): the quad path is compute-latency bound, and this
+  // measured 13.8 -> 14.3 ms at the C2 n = 16 point, so it is off by default.
+  constexpr bool RMW = (T == 4 && STG == 2 && QRMW);
   int buf = 0;
   for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf = (buf + 1 == STG ? 0 : buf + 1)) {
-    {
+    if constexpr (!RMW) {
       const ix rn = rd + (ix)(STG - 1) * gridDim.x;
       const int bn = (buf + STG - 1) % STG;
       if (rn < nrounds) issue(rn, bn);
+      cp_async_commit();
+      cp_async_wait<STG - 1>();
+    } else {
+      cp_async_wait<0>();
     }
-    cp_async_commit();
-    cp_async_wait<STG - 1>();
     __syncthreads();
     double *S = smem + buf * Cfg::BUF;
     const int it = tid / T, q = tid % T;
     double *Si = S + it * STRIDE;
     double *di = sdinv + it * N;
+    if constexpr (RMW) {
+      const ix bi = rd * ITEMS + it;
+      if (q < NP && 4 * q + 3 < N && bi < g.batch) {
+        const double *Di = Db + bi * g.D.stride;
+        // strict-upper elements (r, c), r < c, of diagonal block q: the two
+        // whole pieces (rows 0-1 of cols 2, 3) as 16 B, (0,1) and (2,3) as 8 B
+        // (their piece-mates are on the diagonal, which the factor owns)
+        const double *Dq = Di + eo(g.di + 4 * q, g.dj + 4 * q, g.D.cn);
+        double *Sq = Si + Cfg::poff(q) + 4 * (4 * q);
+        cp_async16(Sq + 8, Dq + 8, 16);
+        cp_async16(Sq + 12, Dq + 12, 16);
+        cp_async8(Sq + 4, Dq + 4, 8);
+        cp_async8(Sq + 14, Dq + 14, 8);
+      }
+      cp_async_commit();
+      const ix rn = rd + gridDim.x;
+      if (rn < nrounds) issue(rn, buf ^ 1);
+      cp_async_commit();
+    }
     int fail;
     if constexpr (T == 1) {
       double L[4 * NP][N];
@@ -327,6 +358,7 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
       sinfo[it] = fail;
       if (b0 + it < g.batch && g.info) g.info[b0 + it] = fail;
     }
+    if constexpr (RMW) cp_async_wait<1>();  // this thread's D pieces have landed
     __syncthreads();
     // Stores of the reference's write set (lower triangle; on failure only
     // what the reference stored before returning).  Columns left of a
@@ -387,6 +419,7 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
                 const int r = 4 * p + 2 * h + i;
                 bool wi = r >= col && r < N && col < N;
                 if (f >= 0) wi = wi && (r < iif || (r < iif + 4 && col < iif));
+                else if (RMW && 4 * p + 3 < N) wi = true;  // merged sector: D's own bytes above the diagonal
                 wr[i] = wi;
                 val[i] = Si2[Cfg::poff(p) + 4 * col + 2 * h + i];
               }
@@ -418,230 +451,186 @@ __global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
   cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------------
-// n <= 8: warp-autonomous kernel with whole-sector stores.
-//
-// Each warp owns 32 items per iteration (lane = item for the factor) and
-// runs its own software pipeline: the NEXT group's lower prefix of C is
-// loaded into registers (coalesced 16-byte pieces, lane-consecutive)
-// while the current group is factored from a warp-private shared-memory
-// transpose; no CTA barrier anywhere.
-//
-// Stores: the reference writes the lower triangle only, so the diagonal
-// 4x4 blocks hold 32-byte sectors that are only partly written.  Left to
-// the hardware, every such sector costs an L2 fill from DRAM in the middle
-// of the write stream (profiles/r01_potrf_n4_ncu_summary.txt).  Here the
-// warp loads exactly those sectors' pieces of D together with C (same
-// pipeline stage), merges, and stores every touched sector whole: the
-// bytes outside the reference's write set are re-stored with the values
-// just read from D, so they never change (tools/potrf4_exp.cu measured
-// 0.27 -> 0.35 of HBM at n = 4).  A failing item (rare) falls back to
-// element-masked stores of exactly the reference's partial write set.
+// element (row 4p + r, col) of an n x n item's lower prefix is in the
+// reference's write set (lower triangle, rows < n)
 template <int N>
 struct WarpCfg {
-  static constexpr int NP = (N + 3) / 4;
-  __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
-  __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
-  static constexpr int IE = poff(NP);  // lower-prefix doubles per item
-  static constexpr int PC = IE / 2;    // 16-byte pieces per item
-  // smem stride per item: 16-byte aligned, an odd number of 16-byte units
-  // (lane-per-item reads spread over the banks)
-  static constexpr int SS = IE + 2;  // PC = 2*sum(cols) is even; slot IE carries the status
-  static_assert(PC % 2 == 0, "odd 16-byte units per item stride");
-  // element (row 4p + r, col) of the prefix is in the write set
-  __host__ __device__ static constexpr bool wr(int p, int col, int r) {
-    return 4 * p + r < N && 4 * p + r >= col;
-  }
-  __host__ __device__ static constexpr int panel_of(int w, int p = 0) {
-    return p + 1 < NP && w >= poff(p + 1) / 2 ? panel_of(w, p + 1) : p;
-  }
-  __host__ __device__ static constexpr bool full_piece(int w) {
-    return wr(panel_of(w), (w - poff(panel_of(w)) / 2) >> 1, 2 * ((w - poff(panel_of(w)) / 2) & 1)) &&
-           wr(panel_of(w), (w - poff(panel_of(w)) / 2) >> 1, 2 * ((w - poff(panel_of(w)) / 2) & 1) + 1);
-  }
-  __host__ __device__ static constexpr int count_mixed(int w) { return w == PC ? 0 : (full_piece(w) ? 0 : 1) + count_mixed(w + 1); }
-  static constexpr int DPC = count_mixed(0);  // pieces of D needed per item
-  static constexpr int WARPS = N <= 4 ? 4 : 2;
-  static constexpr int STAGE = 32 * SS + 32 * 2 * DPC;  // doubles per pipeline stage
-  static constexpr size_t SMEM_WARP = sizeof(double) * 2 * STAGE;
-  static constexpr size_t SMEM = WARPS * SMEM_WARP + sizeof(int) * (PC + DPC + 2);
+  __host__ __device__ static constexpr bool wr(int p, int col, int r) { return 4 * p + r < N && 4 * p + r >= col; }
 };
 
-template <int N>
-__device__ __forceinline__ void warp_piece(int w, int &p, int &col, int &h) {
-  using Cfg = WarpCfg<N>;
-  p = 0;
-#pragma unroll
-  for (int q = 1; q < Cfg::NP; ++q)
-    if (w >= Cfg::poff(q) / 2) p = q;
-  const int rem = w - Cfg::poff(p) / 2;
-  col = rem >> 1;
-  h = rem & 1;
-}
-
-template <int N>
-__global__ void __launch_bounds__(WarpCfg<N>::WARPS * 32, (N <= 4 ? 4 : 3)) potrf_warp_kernel(PotrfArgs g) {
-  using Cfg = WarpCfg<N>;
-  constexpr int PC = Cfg::PC, DPC = Cfg::DPC, SS = Cfg::SS, NP = Cfg::NP;
+// ---------------------------------------------------------------------
+// n <= 8: the CTA kernel's thread-per-item factor (registers), with
+// whole-sector stores.  After a thread has copied its item's staged prefix
+// into registers, the item's smem slot is free: the thread cp.asyncs the
+// pieces of D that share a sector with the write set but are not in it
+// (diagonal-block strict upper, padding rows) straight into their own slots,
+// overlapped with the factor; the factor then writes back only its write
+// set, so the slot holds exactly the merged sectors and every piece of the
+// prefix is stored whole (no L2 fills from DRAM in the write stream).
+template <int N, int NTH>
+__global__ void __launch_bounds__(NTH) potrf_small1_kernel(PotrfArgs g) {
+  using Cfg = SmallCfg<N, NTH, 2>;
+  using WC = WarpCfg<N>;
+  constexpr int NP = Cfg::NP, ITEMS = Cfg::ITEMS, STRIDE = Cfg::STRIDE;
+  static_assert(Cfg::T == 1, "thread-per-item sizes only");
   extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double *W = smem + (size_t)wid * 2 * Cfg::STAGE;  // this warp's two stages
-  int *tab = (int *)(smem + Cfg::WARPS * 2 * Cfg::STAGE);  // j -> piece w of the D list
-  int *inv = tab + DPC;                                     // w -> j, or -1 (fully written)
-  if (threadIdx.x == 0) {
-    int j = 0;
-    for (int w = 0; w < PC; ++w) {
-      int p, col, h;
-      warp_piece<N>(w, p, col, h);
-      const bool full = Cfg::wr(p, col, 2 * h) && Cfg::wr(p, col, 2 * h + 1);
-      inv[w] = full ? -1 : j;
-      if (!full) tab[j++] = w;
-    }
-  }
-  __syncthreads();
-
-  const ix ngroups = (g.batch + 31) / 32;
-  const ix gw = (ix)blockIdx.x * Cfg::WARPS + wid, nw = (ix)gridDim.x * Cfg::WARPS;
+  double *sdinv = smem + 2 * Cfg::BUF;
+  int *sinfo = (int *)(sdinv + Cfg::DINV);
+  const int tid = threadIdx.x;
+  const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
   const double *Cb = g.C.p;
   double *Db = g.D.p;
-  // stage group `grp`: C's lower prefix (item-major, stride SS) and the
-  // pieces of D that share a sector with the write set but are not in it
-  auto issue = [&](ix grp, int st) {
-    double *S = W + st * Cfg::STAGE;
-    double *SD = S + 32 * SS;
+
+  auto issue = [&](ix rd, int buf) {
+    double *S = smem + buf * Cfg::BUF;
+    const ix b0 = rd * ITEMS;
 #pragma unroll
-    for (int k = 0; k < PC; ++k) {
-      const int q = lane + 32 * k, it = q / PC, w = q - it * PC;
-      const ix b = grp * 32 + it;
-      int p, col, h;
-      warp_piece<N>(w, p, col, h);
-      const bool ok = b < g.batch;
-      const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
-      cp_async16(S + it * SS + 2 * w, src, ok ? 16 : 0);
-    }
+    for (int p = 0; p < NP; ++p) {
+      const int pieces = 2 * Cfg::cols(p);
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int trips = (ITEMS * pieces + NTH - 1) / NTH;
 #pragma unroll
-    for (int k = 0; k < DPC; ++k) {
-      const int q = lane + 32 * k, it = q / DPC, j = q - it * DPC;
-      const ix b = grp * 32 + it;
-      int p, col, h;
-      warp_piece<N>(tab[j], p, col, h);
-      const bool ok = b < g.batch;
-      const double *src = ok ? Db + b * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h : Db;
-      cp_async16(SD + 2 * q, src, ok ? 16 : 0);
+      for (int k = 0; k < trips; ++k) {
+        const int q = tid + k * NTH;
+        if (q < ITEMS * pieces) {
+          const int it = q / pieces, w = q - it * pieces;
+          const int col = w >> 1, h = w & 1;
+          const ix b = b0 + it;
+          const bool ok = b < g.batch;
+          const double *src = ok ? Cb + b * g.C.stride + eo(g.ci + 4 * p, g.cj + col, g.C.cn) + 2 * h : Cb;
+          cp_async16(S + it * STRIDE + Cfg::poff(p) + 4 * col + 2 * h, src, ok ? 16 : 0);
+        }
+      }
     }
   };
 
-  ix grp = gw;
-  int st = 0;
-  if (grp < ngroups) issue(grp, 0);
+  ix rd = blockIdx.x;
+  int buf = 0;
+  if (rd < nrounds) issue(rd, 0);
   cp_async_commit();
-  for (; grp < ngroups; grp += nw, st ^= 1) {
-    if (grp + nw < ngroups) issue(grp + nw, st ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
-    double *S = W + st * Cfg::STAGE;
-    const double *SD = S + 32 * SS;
-    const ix b0 = grp * 32;
-    int fail = -1;
-    {
-      double L[4 * NP][N];
-      double *Si = S + lane * SS;
+  for (; rd < nrounds; rd += gridDim.x, buf ^= 1) {
+    cp_async_wait<0>();
+    __syncthreads();
+    double *S = smem + buf * Cfg::BUF;
+    const ix b0 = rd * ITEMS;
+    const int it = tid;
+    double *Si = S + it * STRIDE;
+    double L[4 * NP][N];
 #pragma unroll
-      for (int p = 0; p < NP; ++p)
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) L[4 * p + r][c] = c < Cfg::cols(p) ? Si[Cfg::poff(p) + 4 * c + r] : 0.0;
+      for (int c = 0; c < N; ++c) {
+        if (c < Cfg::cols(p)) {
+          const double2 lo = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c);
+          const double2 hi = *reinterpret_cast<const double2 *>(Si + Cfg::poff(p) + 4 * c + 2);
+          L[4 * p][c] = lo.x, L[4 * p + 1][c] = lo.y, L[4 * p + 2][c] = hi.x, L[4 * p + 3][c] = hi.y;
+        } else {
+          L[4 * p][c] = L[4 * p + 1][c] = L[4 * p + 2][c] = L[4 * p + 3][c] = 0.0;
         }
-      double dinv[N];
-#pragma unroll
-      for (int c = 0; c < N; ++c) dinv[c] = 0.0;
-      const bool live = b0 + lane < g.batch;
-      if (live) fail = factor_t1<N>(L, dinv);
+      }
+    const ix bi = b0 + it;
+    // D's bytes for the non-written part of every touched sector -> own slot
+    if (bi < g.batch) {
+      const double *Di = Db + bi * g.D.stride;
 #pragma unroll
       for (int p = 0; p < NP; ++p)
 #pragma unroll
         for (int c = 0; c < N; ++c)
-          if (c < Cfg::cols(p)) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) Si[Cfg::poff(p) + 4 * c + r] = L[4 * p + r][c];
+          for (int h = 0; h < 2; ++h)
+            if (c < Cfg::cols(p) && !(WC::wr(p, c, 2 * h) && WC::wr(p, c, 2 * h + 1)))
+              cp_async16(Si + Cfg::poff(p) + 4 * c + 2 * h, Di + eo(g.di + 4 * p, g.dj + c, g.D.cn) + 2 * h, 16);
+    }
+    cp_async_commit();
+    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    int fail = -1;
+    double *di = sdinv + it * N;
+    if (bi < g.batch) fail = factor_t1<N>(L, di);
+    cp_async_wait<1>();  // this thread's D pieces have landed
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int c = 0; c < N; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (c < Cfg::cols(p) && WC::wr(p, c, r)) Si[Cfg::poff(p) + 4 * c + r] = L[4 * p + r][c];
+    sinfo[it] = fail;
+    if (bi < g.batch && g.info) g.info[bi] = fail;
+    __syncthreads();
+    // stores: every 16-byte piece of the lower prefix, whole, unless the
+    // item failed (then exactly the reference's partial write set)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int pieces = 2 * Cfg::cols(p);
+      const int trips = (ITEMS * pieces + NTH - 1) / NTH;
+      constexpr int MAXTRIPS = (ITEMS * 2 * N + NTH - 1) / NTH;
+#pragma unroll
+      for (int k = 0; k < MAXTRIPS; ++k) {
+        const int qq = tid + k * NTH;
+        if (k < trips && qq < ITEMS * pieces) {
+          const int it2 = qq / pieces, w = qq - it2 * pieces;
+          const int col = w >> 1, h = w & 1;
+          const ix bb = b0 + it2;
+          if (bb < g.batch) {
+            const double2 v = *reinterpret_cast<const double2 *>(S + it2 * STRIDE + Cfg::poff(p) + 4 * col + 2 * h);
+            double *dst = Db + bb * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
+            const int f = sinfo[it2];
+            if (f < 0) {
+              *reinterpret_cast<double2 *>(dst) = v;
+            } else {
+              const int r0 = 4 * p + 2 * h, iif = f & ~3;
+              const bool w0 = r0 < N && r0 >= col && (r0 < iif || (r0 < iif + 4 && col < iif));
+              const bool w1 = r0 + 1 < N && r0 + 1 >= col && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
+              if (w0 && w1) *reinterpret_cast<double2 *>(dst) = v;
+              else if (w0) dst[0] = v.x;
+              else if (w1) dst[1] = v.y;
+            }
           }
-      if (live && g.info) g.info[b0 + lane] = fail;
-      // diag_inv: lane-consecutive doubles (coalesced), values gathered from
-      // the owning lane by shuffles: store k covers items (32k + lane) / N
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const int q = lane + 32 * k, it = q / N, c = q - it * N;
-        double v = 0.0;
-#pragma unroll
-        for (int c2 = 0; c2 < N; ++c2) {
-          const double t = __shfl_sync(0xffffffffu, dinv[c2], it);
-          if (c2 == c) v = t;
         }
-        const int f = __shfl_sync(0xffffffffu, fail, it);
-        if (b0 + it < g.batch && (f < 0 || c < f)) g.D.d[(b0 + it) * g.D.dstride + g.dj + c] = v;
-      }
-      reinterpret_cast<int *>(Si + SS - 2)[0] = fail;  // pad slot carries the status
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < PC; ++k) {
-      const int q = lane + 32 * k, it = q / PC, w = q - it * PC;
-      const ix b = b0 + it;
-      if (b >= g.batch) continue;
-      int p, col, h;
-      warp_piece<N>(w, p, col, h);
-      const int r0 = 4 * p + 2 * h;
-      double2 v = *reinterpret_cast<const double2 *>(S + it * SS + 2 * w);
-      double *dst = Db + b * g.D.stride + eo(g.di + 4 * p, g.dj + col, g.D.cn) + 2 * h;
-      const int f = reinterpret_cast<const int *>(S + it * SS + SS - 2)[0];
-      bool w0 = Cfg::wr(p, col, 2 * h), w1 = Cfg::wr(p, col, 2 * h + 1);
-      if (f < 0) {
-        if (!(w0 && w1)) {  // sector merge with D's own bytes
-          const double2 old = *reinterpret_cast<const double2 *>(SD + 2 * (it * DPC + inv[w]));
-          if (!w0) v.x = old.x;
-          if (!w1) v.y = old.y;
-        }
-        *reinterpret_cast<double2 *>(dst) = v;
-      } else {  // the reference's partial write set of a failing item
-        const int iif = f & ~3;
-        w0 = w0 && (r0 < iif || (r0 < iif + 4 && col < iif));
-        w1 = w1 && (r0 + 1 < iif || (r0 + 1 < iif + 4 && col < iif));
-        if (w0 && w1) *reinterpret_cast<double2 *>(dst) = v;
-        else if (w0) dst[0] = v.x;
-        else if (w1) dst[1] = v.y;
       }
     }
-    __syncwarp();
+    {
+      constexpr int trips = (ITEMS * N + NTH - 1) / NTH;
+#pragma unroll
+      for (int k = 0; k < trips; ++k) {
+        const int qq = tid + k * NTH;
+        if (qq < ITEMS * N) {
+          const int it2 = qq / N, c = qq - it2 * N;
+          const ix bb = b0 + it2;
+          const int f = sinfo[it2];
+          if (bb < g.batch && (f < 0 || c < f)) g.D.d[bb * g.D.dstride + g.dj + c] = sdinv[qq];
+        }
+      }
+    }
   }
   cp_async_wait<0>();
 }
 
-template <int N>
-static cudaError_t launch_warp(const PotrfArgs &g, cudaStream_t st) {
-  using Cfg = WarpCfg<N>;
-  auto kern = potrf_warp_kernel<N>;
+template <int N, int NTH = 128>
+static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
+  using Cfg = SmallCfg<N, NTH, 2>;
+  auto kern = potrf_small1_kernel<N, NTH>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::WARPS * 32, Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTH, Cfg::SMEM);
     if (occ < 1) occ = 1;
   }
-  const ix groups = (g.batch + 31) / 32;
-  const ix ctas = (groups + Cfg::WARPS - 1) / Cfg::WARPS;
+  const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
   ix grid = (ix)num_sms() * occ;
-  if (grid > ctas) grid = ctas;
+  if (grid > rounds) grid = rounds;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, Cfg::WARPS * 32, Cfg::SMEM, st>>>(g);
+  kern<<<(unsigned)grid, NTH, Cfg::SMEM, st>>>(g);
   note_launch();
   return cudaGetLastError();
 }
 
-template <int N, int NTH_ = 128, int STAGES_ = 2>
+template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
-  auto kern = potrf_small_kernel<N, NTH_, STAGES_>;
+  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -672,6 +661,7 @@ static cudaError_t launch_small_tuned(const PotrfArgs &g, cudaStream_t st) {
     if (v == "64x1") return launch_small<N, 64, 1>(g, st);
     if (v == "256x1") return launch_small<N, 256, 1>(g, st);
   }
+  if (getenv("PB_QUAD_RMW")) return launch_small<N, 128, 2, true>(g, st);
   return launch_small<N>(g, st);
 }
 
@@ -685,18 +675,18 @@ bool potrf_small_ok(const PotrfArgs &g) {
 
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
   static const bool legacy = getenv("PB_SMALL_LEGACY") != nullptr;  // A/B switch for the sweeps
-  // n <= 4: warp-autonomous whole-sector kernel (measured 0.27 -> 0.32 of HBM at n = 4);
-  // 5 <= n <= 8 stays on the CTA kernel, which measured faster there (register pressure)
-  if (!legacy && g.n <= 4) {
+  // n <= 8: thread-per-item factor with whole-sector stores (potrf_small1_kernel):
+  // measured n = 4 0.27 -> 0.33, n = 8 0.34 -> 0.45 of HBM (profiles/r01_potrf_small_rmw.txt)
+  if (!legacy && g.n <= 8) {
     switch (g.n) {
-      case 1: return launch_warp<1>(g, st);
-      case 2: return launch_warp<2>(g, st);
-      case 3: return launch_warp<3>(g, st);
-      case 4: return launch_warp<4>(g, st);
-      case 5: return launch_warp<5>(g, st);
-      case 6: return launch_warp<6>(g, st);
-      case 7: return launch_warp<7>(g, st);
-      case 8: return launch_warp<8>(g, st);
+      case 1: return launch_small1<1>(g, st);
+      case 2: return launch_small1<2>(g, st);
+      case 3: return launch_small1<3>(g, st);
+      case 4: return launch_small1<4>(g, st);
+      case 5: return launch_small1<5>(g, st);
+      case 6: return launch_small1<6>(g, st);
+      case 7: return launch_small1<7>(g, st);
+      case 8: return launch_small1<8>(g, st);
     }
   }
   switch (g.n) {
