@@ -237,8 +237,8 @@ __device__ __forceinline__ int factor_t4s(double *Si, double *dinv, int q, volat
   return fail;
 }
 
-template <int N, int NTH_, int STAGES_, bool QRMW = false>
-__global__ void __launch_bounds__(NTH_) potrf_small_kernel(PotrfArgs g) {
+template <int N, int NTH_, int STAGES_, bool QRMW = false, int MINB = 1>
+__global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
   constexpr int STG = Cfg::STAGES;
   constexpr int NP = Cfg::NP, T = Cfg::T, ITEMS = Cfg::ITEMS, STRIDE = Cfg::STRIDE, NTH = Cfg::NTHREADS;
@@ -627,10 +627,10 @@ static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false>
+template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 1>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
-  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW>;
+  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -644,6 +644,16 @@ static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   kern<<<(unsigned)grid, Cfg::NTHREADS, Cfg::SMEM, st>>>(g);
   note_launch();
   return cudaGetLastError();
+}
+
+// Default shape.  The quad path (9 <= n <= 16) is latency bound (FP64
+// dependency chains, 2 warps per scheduler at 246 registers): single-stage
+// 64-thread CTAs capped at 128 registers put 16 warps on an SM and measured
+// best (n = 16: 13.84 -> 11.46 ms, profiles/r01_potrf_small_rmw.txt).
+template <int N>
+static cudaError_t launch_small_default(const PotrfArgs &g, cudaStream_t st) {
+  if constexpr (SmallCfg<N>::T == 4) return launch_small<N, 64, 1, false, 8>(g, st);
+  else return launch_small<N>(g, st);
 }
 
 // tuning hook for the benchmark sweeps (PB_SMALL_CFG = <threads>x<stages>)
@@ -660,9 +670,17 @@ static cudaError_t launch_small_tuned(const PotrfArgs &g, cudaStream_t st) {
     if (v == "128x1") return launch_small<N, 128, 1>(g, st);
     if (v == "64x1") return launch_small<N, 64, 1>(g, st);
     if (v == "256x1") return launch_small<N, 256, 1>(g, st);
+    if (v == "128x1m4") return launch_small<N, 128, 1, false, 4>(g, st);
+    if (v == "128x1m3") return launch_small<N, 128, 1, false, 3>(g, st);
+    if (v == "64x2m5") return launch_small<N, 64, 2, false, 5>(g, st);
+    if (v == "64x1m8") return launch_small<N, 64, 1, false, 8>(g, st);
+    if (v == "256x1m2") return launch_small<N, 256, 1, false, 2>(g, st);
+    if (v == "32x1m16") return launch_small<N, 32, 1, false, 16>(g, st);
+    if (v == "64x2m6") return launch_small<N, 64, 2, false, 6>(g, st);
+    if (v == "32x2m12") return launch_small<N, 32, 2, false, 12>(g, st);
   }
   if (getenv("PB_QUAD_RMW")) return launch_small<N, 128, 2, true>(g, st);
-  return launch_small<N>(g, st);
+  return launch_small_default<N>(g, st);
 }
 
 bool potrf_small_ok(const PotrfArgs &g) {
@@ -692,7 +710,7 @@ cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
   switch (g.n) {
 #define PB_SMALL(N_) \
   case N_:           \
-    return launch_small<N_>(g, st);
+    return launch_small_default<N_>(g, st);
     PB_SMALL(1) PB_SMALL(2) PB_SMALL(3) PB_SMALL(5) PB_SMALL(6) PB_SMALL(7)
     PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15)
 #undef PB_SMALL
