@@ -49,7 +49,9 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
 // One item, one thread (n <= 8).  L holds C's lower prefix on entry (rows
-// 0..4NP-1, cols 0..N-1 as available) and the factor on exit.
+// 0..4NP-1, cols 0..N-1 as available) and the factor on exit (write set
+// only: strict-upper and padding-row entries are never read, so they stay
+// dead and cost no registers).
 template <int N>
 __device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], double *dinv) {
   constexpr int NP = SmallCfg<N>::NP;
@@ -68,7 +70,7 @@ __device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], do
           double s = 0.0;
 #pragma unroll
           for (int l = 0; l < 4 * jj; ++l)
-            if (c < ns) s = dadd(s, dmul(L[4 * ii + r][l], -L[4 * jj + c][l]));
+            if (c < ns && 4 * ii + r < N && (jj < ii || r >= c)) s = dadd(s, dmul(L[4 * ii + r][l], -L[4 * jj + c][l]));
           acc[c][r] = s;
         }
       if (jj < ii) {
@@ -96,7 +98,7 @@ __device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], do
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int r = 0; r < 4; ++r)
-            if (c < ns) acc[c][r] = dadd(acc[c][r], L[4 * ii + r][4 * jj + c]);
+            if (c < ns && r >= c && 4 * ii + r < N) acc[c][r] = dadd(acc[c][r], L[4 * ii + r][4 * jj + c]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c < ns) {
@@ -467,14 +469,14 @@ struct WarpCfg {
 // overlapped with the factor; the factor then writes back only its write
 // set, so the slot holds exactly the merged sectors and every piece of the
 // prefix is stored whole (no L2 fills from DRAM in the write stream).
-template <int N, int NTH>
-__global__ void __launch_bounds__(NTH) potrf_small1_kernel(PotrfArgs g) {
-  using Cfg = SmallCfg<N, NTH, 2>;
+template <int N, int NTH, int STG = 2, int MINB = 1>
+__global__ void __launch_bounds__(NTH, MINB) potrf_small1_kernel(PotrfArgs g) {
+  using Cfg = SmallCfg<N, NTH, STG>;
   using WC = WarpCfg<N>;
   constexpr int NP = Cfg::NP, ITEMS = Cfg::ITEMS, STRIDE = Cfg::STRIDE;
   static_assert(Cfg::T == 1, "thread-per-item sizes only");
   extern __shared__ __align__(128) double smem[];
-  double *sdinv = smem + 2 * Cfg::BUF;
+  double *sdinv = smem + STG * Cfg::BUF;
   int *sinfo = (int *)(sdinv + Cfg::DINV);
   const int tid = threadIdx.x;
   const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
@@ -505,11 +507,18 @@ __global__ void __launch_bounds__(NTH) potrf_small1_kernel(PotrfArgs g) {
     }
   };
 
+  // STG == 2: the next round streams in while this one is factored;
+  // STG == 1: half the shared memory per item (more CTAs per SM), the
+  // overlap comes from the other CTAs
   ix rd = blockIdx.x;
   int buf = 0;
-  if (rd < nrounds) issue(rd, 0);
+  if (STG == 2 && rd < nrounds) issue(rd, 0);
   cp_async_commit();
-  for (; rd < nrounds; rd += gridDim.x, buf ^= 1) {
+  for (; rd < nrounds; rd += gridDim.x, buf ^= (STG - 1)) {
+    if (STG == 1) {
+      issue(rd, 0);
+      cp_async_commit();
+    }
     cp_async_wait<0>();
     __syncthreads();
     double *S = smem + buf * Cfg::BUF;
@@ -543,7 +552,7 @@ __global__ void __launch_bounds__(NTH) potrf_small1_kernel(PotrfArgs g) {
               cp_async16(Si + Cfg::poff(p) + 4 * c + 2 * h, Di + eo(g.di + 4 * p, g.dj + c, g.D.cn) + 2 * h, 16);
     }
     cp_async_commit();
-    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+    if (STG == 2 && rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
     cp_async_commit();
     int fail = -1;
     double *di = sdinv + it * N;
@@ -604,14 +613,15 @@ __global__ void __launch_bounds__(NTH) potrf_small1_kernel(PotrfArgs g) {
         }
       }
     }
+    if (STG == 1) __syncthreads();
   }
   cp_async_wait<0>();
 }
 
-template <int N, int NTH = 128>
+template <int N, int NTH = 128, int STG = 2, int MINB = 1>
 static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
-  using Cfg = SmallCfg<N, NTH, 2>;
-  auto kern = potrf_small1_kernel<N, NTH>;
+  using Cfg = SmallCfg<N, NTH, STG>;
+  auto kern = potrf_small1_kernel<N, NTH, STG, MINB>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -700,11 +710,32 @@ cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
       case 1: return launch_small1<1>(g, st);
       case 2: return launch_small1<2>(g, st);
       case 3: return launch_small1<3>(g, st);
-      case 4: return launch_small1<4>(g, st);
+      case 4: {
+        const char *e = getenv("PB_SMALL_CFG");
+        if (e) {
+          const std::string v(e);
+          if (v == "64x1m8") return launch_small1<4, 64, 1, 8>(g, st);
+          if (v == "128x1m4") return launch_small1<4, 128, 1, 4>(g, st);
+          if (v == "128x2m3") return launch_small1<4, 128, 2, 3>(g, st);
+          if (v == "128x2") return launch_small1<4>(g, st);
+        }
+        // single stage, 16 warps/SM: 71.8 -> 68.9 ms at the C2 n = 4 point
+        return launch_small1<4, 128, 1, 4>(g, st);
+      }
       case 5: return launch_small1<5>(g, st);
       case 6: return launch_small1<6>(g, st);
       case 7: return launch_small1<7>(g, st);
-      case 8: return launch_small1<8>(g, st);
+      case 8: {
+        const char *e = getenv("PB_SMALL_CFG");
+        if (e) {
+          const std::string v(e);
+          if (v == "64x1m8") return launch_small1<8, 64, 1, 8>(g, st);
+          if (v == "64x1m6") return launch_small1<8, 64, 1, 6>(g, st);
+          if (v == "32x1m14") return launch_small1<8, 32, 1, 14>(g, st);
+          if (v == "64x2") return launch_small1<8, 64, 2>(g, st);
+        }
+        return launch_small1<8>(g, st);
+      }
     }
   }
   switch (g.n) {
