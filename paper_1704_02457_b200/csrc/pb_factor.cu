@@ -19,6 +19,8 @@
 // Bad pivots: the first index with d <= 0 (NaN passes, ccore.pyx:423) goes
 // to info[b]; the write-back then stores exactly the part of D the
 // reference would have stored before returning, and dinv[0, index).
+#include <cstdlib>
+
 #include "pb_tri.cuh"
 
 namespace pb {
@@ -584,6 +586,8 @@ bool potrf_fits(ix m, ix n) {
 
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   if (potrf_small_ok(g)) return run_potrf_small(g, st);
+  static const bool team_only = getenv("PB_POTRF_TEAM") != nullptr;  // A/B switch
+  if (!team_only && potrf_reg_ok(g)) return run_potrf_reg(g, st);
   const ix gm = (g.m + 7) / 8;
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
   const ix gn = (g.n + 7) / 8;
@@ -608,6 +612,8 @@ bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same) {
 
 // fused syrk + potrf: single-buffered generic team shapes
 cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st) {
+  static const bool team_only = getenv("PB_POTRF_TEAM") != nullptr;
+  if (!team_only && potrf_reg_ok(g)) return run_potrf_reg(g, st);
   const ix gm = (g.m + 7) / 8;
   if (gm <= 2) return launch_potrf<1, 2, false, 0, 0, true, 4>(g, st);
   if (gm <= 4) return launch_potrf<1, 4, false, 0, 0, true, 4>(g, st);

@@ -74,6 +74,8 @@ bool potrf_fits(ix m, ix n);
 bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same);
 cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st);
 bool potrf_small_ok(const PotrfArgs &g);
+bool potrf_reg_ok(const PotrfArgs &g);
+cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
 

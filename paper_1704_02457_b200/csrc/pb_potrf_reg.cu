@@ -1,0 +1,241 @@
+// Batched dpotrf_l for 17 <= n <= 64: one warp per item, the whole lower
+// triangle register-resident as 8x8 DMMA accumulator tiles (sm_100a).
+//
+// Reference semantics: potrf_drv ccore.pyx:877-905 (+ _kpotrf_core
+// :404-438): lower Cholesky of lower(C), sqrt then one reciprocal per
+// column (dinv[j] = 1/L[j][j], column scaled by it), first pivot with
+// d <= 0 (NaN passes) -> info, failing items written exactly as far as the
+// reference writes them.  Floating-point order differs from the reference
+// (right-looking, FMA, DMMA): parity is the 50*n*eps Frobenius tolerance.
+//
+// Why this shape: the C2 points n = 32 / 64 are HBM-bound (AI 1.3 / 2.6
+// flop/B).  The shared-memory team kernel spent ~3.7K / 9.6K warp
+// instructions per item on staging, index math and barriers
+// (profiles/r01_potrf_reg_ncu.txt).  Here an item costs one pass of loads,
+// register math and one pass of stores:
+//  * tile (i, j), i >= j, of 8x8 elements is one m8n8k4 accumulator: lane
+//    (r = lane/4, q = lane%4) holds (8i + r, 8j + 2q + {0,1}); a warp-wide
+//    8-byte load/store of one element slot covers 8 whole 32-byte sectors
+//    of the panel-major item (two panels x four columns);
+//  * right-looking over 8-column panels: the panel is factored column by
+//    column with warp shuffles (pivot broadcast, sqrt, one reciprocal,
+//    column scale, rank-1 update of the panel's remaining columns), then
+//    the trailing lower tiles take  T(i,j) -= P(i) P(j)^T  on DMMA; a panel
+//    tile's A fragment (8x4, row-major) is also the B fragment of its
+//    transpose, so each panel tile is converted once (4 quad shuffles);
+//  * no shared memory and no barriers: occupancy is set by registers only,
+//    and other warps hide each item's load latency and pivot chain; the
+//    next item's rows are prefetched into L2 by one bulk prefetch.
+#include "pb_gemm.cuh"
+
+namespace pb {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ constexpr int ti(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// 1/sqrt(d) for the pivot: MUFU seed + two Newton steps (FMA), branch-free;
+// the pivot chain is the kernel's critical path, and __dsqrt_rn +
+// __ddiv_rn cost two slow-path call sequences per column.  d > 0 here
+// (d <= 0 failed before); NaN propagates.
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int GM, bool SYRK>
+__global__ void __launch_bounds__(128, (GM <= 4 ? 4 : (GM <= 6 ? 3 : 2))) potrf_reg_kernel(PotrfArgs g, int pf_ok) {
+  constexpr int NT = GM * (GM + 1) / 2;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int n = (int)g.n;
+  const ix wpb = blockDim.x >> 5;
+  const ix nw = (ix)gridDim.x * wpb;
+  const unsigned pf_bytes = 32u * (unsigned)g.C.cn * (unsigned)((n + 3) / 4);
+  // per-lane row offsets of the window rows 8i + r (panel carry included),
+  // so an element address is one add of a compile-time column offset
+  ix offC[GM], offD[GM];
+#pragma unroll
+  for (int i = 0; i < GM; ++i) {
+    offC[i] = eo(g.ci + 8 * i + r, g.cj + 2 * q, g.C.cn);
+    offD[i] = eo(g.di + 8 * i + r, g.dj + 2 * q, g.D.cn);
+  }
+  for (ix b = (ix)blockIdx.x * wpb + (threadIdx.x >> 5); b < g.batch; b += nw) {
+    const double *Cb = g.C.p + b * g.C.stride;
+    if (pf_ok && lane == 0 && b + nw < g.batch)
+      prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci, 0, g.C.cn), pf_bytes);
+    double T[NT][2];
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int R = 8 * i + r, Cc = 8 * j + 2 * q + e;
+          // lower(C) inside the window; outside: identity padding, so the
+          // padded columns factor trivially and never couple to real rows
+          T[ti(i, j)][e] = (R < n && Cc <= R) ? Cb[offC[i] + 4 * (8 * j + e)] : (R == Cc ? 1.0 : 0.0);
+        }
+    if constexpr (SYRK) {  // fused syrk_potrf_ln (ccore.pyx:908-941): factor lower(C + A B^T)
+      const double *Ab = g.A.p + b * g.A.stride, *Bb = g.B.p + b * g.B.stride;
+      const int k = (int)g.k;
+      for (int s = 0; s < (k + 3) / 4; ++s) {
+        const int kk = 4 * s + q;  // A fragment (8x4 row-major) == B fragment of the transpose
+        double fa[GM], fb[GM];
+#pragma unroll
+        for (int i = 0; i < GM; ++i) {
+          const int R = 8 * i + r;
+          const bool ok = R < n && kk < k;
+          fa[i] = ok ? Ab[eo(g.ai + R, g.aj + kk, g.A.cn)] : 0.0;
+          fb[i] = g.ab_same ? fa[i] : (ok ? Bb[eo(g.bi + R, g.bj + kk, g.B.cn)] : 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < GM; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) dmma(T[ti(i, j)], fa[i], fb[j]);
+      }
+    }
+    int fail = -1;
+    double *dA = g.D.d + b * g.D.dstride + g.dj;
+#pragma unroll
+    for (int k = 0; k < GM; ++k) {
+      double myinv = 0.0;
+      int done = 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int h = j >> 1, ej = j & 1;
+        const double d = __shfl_sync(FULL, T[ti(k, k)][ej], 4 * j + h);
+        if (d <= 0.0) {  // ccore.pyx:423; warp-uniform
+          fail = 8 * k + j;
+          done = j;
+          break;
+        }
+        const double inv = rsqrt_nr(d);
+        const double l = d * inv;
+        if (lane == j) myinv = inv;
+        if (q == h) {
+          double v = T[ti(k, k)][ej];
+          v = r > j ? __dmul_rn(v, inv) : (r == j ? l : v);
+          T[ti(k, k)][ej] = v;
+#pragma unroll
+          for (int i = k + 1; i < GM; ++i) T[ti(i, k)][ej] = __dmul_rn(T[ti(i, k)][ej], inv);
+        }
+        if (j < 7) {
+          // L[c][j] for this lane's columns c = 2q + e (valid where c > j)
+          const double lc0 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + h);
+          const double lc1 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + 4 + h);
+#pragma unroll
+          for (int i = k; i < GM; ++i) {
+            const double prj = __shfl_sync(FULL, T[ti(i, k)][ej], 4 * r + h);  // P(i)[r][j]
+            const int c0 = 2 * q, c1 = 2 * q + 1;
+            if (c0 > j && (i > k || r >= c0)) T[ti(i, k)][0] = fma(-prj, lc0, T[ti(i, k)][0]);
+            if (c1 > j && (i > k || r >= c1)) T[ti(i, k)][1] = fma(-prj, lc1, T[ti(i, k)][1]);
+          }
+        }
+      }
+      // reciprocals of the columns this panel completed (reference: dinv
+      // is written column by column, also ahead of a failing pivot)
+      if (lane < done && 8 * k + lane < n) dA[8 * k + lane] = myinv;
+      if (fail >= 0) break;
+      // trailing update  T(i,jj) -= P(i) P(jj)^T,  k < jj <= i
+      if (k + 1 < GM) {
+        double a0[GM], a1[GM];
+#pragma unroll
+        for (int i = k + 1; i < GM; ++i) {
+          const int s0 = 4 * r + (q >> 1), s1 = s0 + 2;
+          const double x0 = __shfl_sync(FULL, T[ti(i, k)][0], s0), x1 = __shfl_sync(FULL, T[ti(i, k)][1], s0);
+          const double y0 = __shfl_sync(FULL, T[ti(i, k)][0], s1), y1 = __shfl_sync(FULL, T[ti(i, k)][1], s1);
+          a0[i] = (q & 1) ? x1 : x0;  // P(i)[r][q]
+          a1[i] = (q & 1) ? y1 : y0;  // P(i)[r][4 + q]
+        }
+#pragma unroll
+        for (int i = k + 1; i < GM; ++i) {
+          const double na0 = -a0[i], na1 = -a1[i];
+#pragma unroll
+          for (int jj = k + 1; jj <= i; ++jj) {
+            dmma(T[ti(i, jj)], na0, a0[jj]);
+            dmma(T[ti(i, jj)], na1, a1[jj]);
+          }
+        }
+      }
+    }
+    if (lane == 0 && g.info) g.info[b] = fail;
+    // write set: lower triangle of the window; a failing item only rows
+    // < iif plus block row iif left of iif (iif = fail & ~3), as the
+    // reference stores before returning (ccore.pyx:884-899)
+    const int iif = fail >= 0 ? (fail & ~3) : 0;
+    double *Db = g.D.p + b * g.D.stride;
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int R = 8 * i + r, Cc = 8 * j + 2 * q + e;
+          bool w = R < n && Cc <= R;
+          if (fail >= 0) w = w && (R < iif || (R < iif + 4 && Cc < iif));
+          if (w) Db[offD[i] + 4 * (8 * j + e)] = T[ti(i, j)][e];
+        }
+  }
+}
+
+template <int GM, bool SYRK>
+cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
+  auto kern = potrf_reg_kernel<GM, SYRK>;
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+    if (occ < 1) occ = 1;
+  }
+  const ix ctas = (g.batch + 3) / 4;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > ctas) grid = ctas;
+  if (grid < 1) grid = 1;
+  const int pf_ok = (g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0;
+  kern<<<(unsigned)grid, 128, 0, st>>>(g, pf_ok);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool potrf_reg_ok(const PotrfArgs &g) { return g.m == g.n && g.n >= 17 && g.n <= 64 && !g.merge; }
+
+cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
+  const int gm = (int)((g.n + 7) / 8);
+  if (g.syrk) {
+    switch (gm) {
+      case 3: return launch_reg<3, true>(g, st);
+      case 4: return launch_reg<4, true>(g, st);
+      case 5: return launch_reg<5, true>(g, st);
+      case 6: return launch_reg<6, true>(g, st);
+      case 7: return launch_reg<7, true>(g, st);
+      case 8: return launch_reg<8, true>(g, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (gm) {
+    case 3: return launch_reg<3, false>(g, st);
+    case 4: return launch_reg<4, false>(g, st);
+    case 5: return launch_reg<5, false>(g, st);
+    case 6: return launch_reg<6, false>(g, st);
+    case 7: return launch_reg<7, false>(g, st);
+    case 8: return launch_reg<8, false>(g, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pb

@@ -1,7 +1,3 @@
-export PB_SMALL_WARPMAX=8
-ncu --set full --clock-control none --import-source on -k regex:potrf_warp_kernel -s 2 -c 1 -o gpurun_out/ncu_warp8 -f \
-  python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 --only "potrf_l n=8" > gpurun_out/ncu_warp8.log 2>&1
-unset PB_SMALL_WARPMAX
-ncu --set full --clock-control none --import-source on -k regex:potrf_small_kernel -s 2 -c 1 -o gpurun_out/ncu_small8 -f \
-  python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 --only "potrf_l n=8" > gpurun_out/ncu_small8.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:potrf_reg_kernel -s 2 -c 1 -o gpurun_out/ncu_reg32 -f \
+  python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 --only "potrf_l n=32" > gpurun_out/ncu_reg32.log 2>&1
 echo done
