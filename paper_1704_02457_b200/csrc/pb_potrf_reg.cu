@@ -55,13 +55,14 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
 }
 
 template <int GM, bool SYRK>
-__global__ void __launch_bounds__(128, (GM <= 4 ? 4 : (GM <= 6 ? 3 : 2))) potrf_reg_kernel(PotrfArgs g, int pf_ok) {
+__global__ void __launch_bounds__(32, (GM <= 4 ? 16 : (GM <= 6 ? 12 : 8))) potrf_reg_kernel(PotrfArgs g, int pf_ok) {
   constexpr int NT = GM * (GM + 1) / 2;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int n = (int)g.n;
-  const ix wpb = blockDim.x >> 5;
-  const ix nw = (ix)gridDim.x * wpb;
+  // one warp per CTA: the item index is CTA-uniform, so the compiler sees
+  // converged control flow around every shuffle and DMMA
+  const ix nw = (ix)gridDim.x;
   const unsigned pf_bytes = 32u * (unsigned)g.C.cn * (unsigned)((n + 3) / 4);
   // per-lane row offsets of the window rows 8i + r (panel carry included),
   // so an element address is one add of a compile-time column offset
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(128, (GM <= 4 ? 4 : (GM <= 6 ? 3 : 2))) potrf_
     offC[i] = eo(g.ci + 8 * i + r, g.cj + 2 * q, g.C.cn);
     offD[i] = eo(g.di + 8 * i + r, g.dj + 2 * q, g.D.cn);
   }
-  for (ix b = (ix)blockIdx.x * wpb + (threadIdx.x >> 5); b < g.batch; b += nw) {
+  for (ix b = (ix)blockIdx.x; b < g.batch; b += nw) {
     const double *Cb = g.C.p + b * g.C.stride;
     if (pf_ok && lane == 0 && b + nw < g.batch)
       prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci, 0, g.C.cn), pf_bytes);
@@ -108,48 +109,55 @@ __global__ void __launch_bounds__(128, (GM <= 4 ? 4 : (GM <= 6 ? 3 : 2))) potrf_
     }
     int fail = -1;
     double *dA = g.D.d + b * g.D.dstride + g.dj;
+    // Control flow stays warp-uniform and branch-free: a failing pivot only
+    // records its index and zeroes its reciprocal (the columns left of it
+    // are final in a right-looking sweep and are never touched again; the
+    // rest is garbage that the write mask drops).
 #pragma unroll
     for (int k = 0; k < GM; ++k) {
       double myinv = 0.0;
-      int done = 8;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         constexpr int dummy = 0;
         (void)dummy;
         const int h = j >> 1, ej = j & 1;
         const double d = __shfl_sync(FULL, T[ti(k, k)][ej], 4 * j + h);
-        if (d <= 0.0) {  // ccore.pyx:423; warp-uniform
-          fail = 8 * k + j;
-          done = j;
-          break;
-        }
-        const double inv = rsqrt_nr(d);
+        const bool bad = d <= 0.0;  // ccore.pyx:423 (NaN passes); warp-uniform
+        if (bad && fail < 0) fail = 8 * k + j;
+        const double inv = bad ? 0.0 : rsqrt_nr(d);
         const double l = d * inv;
         if (lane == j) myinv = inv;
-        if (q == h) {
-          double v = T[ti(k, k)][ej];
-          v = r > j ? __dmul_rn(v, inv) : (r == j ? l : v);
-          T[ti(k, k)][ej] = v;
-#pragma unroll
-          for (int i = k + 1; i < GM; ++i) T[ti(i, k)][ej] = __dmul_rn(T[ti(i, k)][ej], inv);
+        // scale column j (lanes q == h, element ej) by multipliers, so the
+        // update is one unconditional DMUL per tile (x1.0 elsewhere is exact)
+        const bool own = q == h;
+        const double sd = (own && r > j) ? inv : 1.0, so = own ? inv : 1.0;
+        {
+          const double v = T[ti(k, k)][ej] * sd;
+          T[ti(k, k)][ej] = (own && r == j) ? l : v;
         }
+#pragma unroll
+        for (int i = k + 1; i < GM; ++i) T[ti(i, k)][ej] *= so;
         if (j < 7) {
-          // L[c][j] for this lane's columns c = 2q + e (valid where c > j)
+          // rank-1 update of the panel's columns c > j: the multiplier L[c][j]
+          // is zeroed in lanes whose column c <= j, so every update is one
+          // unconditional FMA (the diagonal tile's strict upper is scratch)
           const double lc0 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + h);
           const double lc1 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + 4 + h);
+          const double m0 = 2 * q > j ? -lc0 : 0.0, m1 = 2 * q + 1 > j ? -lc1 : 0.0;
 #pragma unroll
           for (int i = k; i < GM; ++i) {
             const double prj = __shfl_sync(FULL, T[ti(i, k)][ej], 4 * r + h);  // P(i)[r][j]
-            const int c0 = 2 * q, c1 = 2 * q + 1;
-            if (c0 > j && (i > k || r >= c0)) T[ti(i, k)][0] = fma(-prj, lc0, T[ti(i, k)][0]);
-            if (c1 > j && (i > k || r >= c1)) T[ti(i, k)][1] = fma(-prj, lc1, T[ti(i, k)][1]);
+            T[ti(i, k)][0] = fma(prj, m0, T[ti(i, k)][0]);
+            T[ti(i, k)][1] = fma(prj, m1, T[ti(i, k)][1]);
           }
         }
       }
-      // reciprocals of the columns this panel completed (reference: dinv
-      // is written column by column, also ahead of a failing pivot)
-      if (lane < done && 8 * k + lane < n) dA[8 * k + lane] = myinv;
-      if (fail >= 0) break;
+      // reciprocals of the completed columns (the reference writes dinv
+      // column by column, also ahead of a failing pivot)
+      {
+        const int c = 8 * k + lane;
+        if (lane < 8 && c < n && (fail < 0 || c < fail)) dA[c] = myinv;
+      }
       // trailing update  T(i,jj) -= P(i) P(jj)^T,  k < jj <= i
       if (k + 1 < GM) {
         double a0[GM], a1[GM];
@@ -197,15 +205,15 @@ cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
   auto kern = potrf_reg_kernel<GM, SYRK>;
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, 0);
     if (occ < 1) occ = 1;
   }
-  const ix ctas = (g.batch + 3) / 4;
+  const ix ctas = g.batch;
   ix grid = (ix)num_sms() * occ;
   if (grid > ctas) grid = ctas;
   if (grid < 1) grid = 1;
   const int pf_ok = (g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0;
-  kern<<<(unsigned)grid, 128, 0, st>>>(g, pf_ok);
+  kern<<<(unsigned)grid, 32, 0, st>>>(g, pf_ok);
   note_launch();
   return cudaGetLastError();
 }
