@@ -585,9 +585,9 @@ bool potrf_fits(ix m, ix n) {
 }
 
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
-  if (potrf_small_ok(g)) return run_potrf_small(g, st);
   static const bool team_only = getenv("PB_POTRF_TEAM") != nullptr;  // A/B switch
   if (!team_only && potrf_reg_ok(g)) return run_potrf_reg(g, st);
+  if (potrf_small_ok(g)) return run_potrf_small(g, st);
   const ix gm = (g.m + 7) / 8;
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
   const ix gn = (g.n + 7) / 8;

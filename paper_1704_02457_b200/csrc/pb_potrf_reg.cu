@@ -26,6 +26,8 @@
 //  * no shared memory and no barriers: occupancy is set by registers only,
 //    and other warps hide each item's load latency and pivot chain; the
 //    next item's rows are prefetched into L2 by one bulk prefetch.
+#include <cstdlib>
+
 #include "pb_gemm.cuh"
 
 namespace pb {
@@ -55,7 +57,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
 }
 
 template <int GM, bool SYRK>
-__global__ void __launch_bounds__(32, (GM <= 4 ? 16 : (GM <= 6 ? 12 : 8))) potrf_reg_kernel(PotrfArgs g, int pf_ok) {
+__global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ? 12 : 8)))) potrf_reg_kernel(PotrfArgs g, int pf_ok) {
   constexpr int NT = GM * (GM + 1) / 2;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
@@ -220,12 +222,17 @@ cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
 
 }  // namespace
 
-bool potrf_reg_ok(const PotrfArgs &g) { return g.m == g.n && g.n >= 17 && g.n <= 64 && !g.merge; }
+// 9 <= n <= 16 stays on the bit-exact quad kernel unless PB_POTRF_REG16 is set (A/B runs)
+bool potrf_reg_ok(const PotrfArgs &g) {
+  static const int lo = getenv("PB_POTRF_REG16") ? 9 : 17;
+  return g.m == g.n && g.n >= lo && g.n <= 64 && !g.merge;
+}
 
 cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
   const int gm = (int)((g.n + 7) / 8);
   if (g.syrk) {
     switch (gm) {
+      case 2: return launch_reg<2, true>(g, st);
       case 3: return launch_reg<3, true>(g, st);
       case 4: return launch_reg<4, true>(g, st);
       case 5: return launch_reg<5, true>(g, st);
@@ -236,6 +243,7 @@ cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
     }
   }
   switch (gm) {
+    case 2: return launch_reg<2, false>(g, st);
     case 3: return launch_reg<3, false>(g, st);
     case 4: return launch_reg<4, false>(g, st);
     case 5: return launch_reg<5, false>(g, st);
