@@ -811,20 +811,30 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
     // square output tile T in {32, 48, 64} minimising the padded tile area
     // (ties -> larger T); k-chunk 40 when it covers k in one chunk.
     // Measured on B200: profiles/r01_gemm_tuning.txt
+    // square output tile T minimising padded tile area x measured cost per
+    // unit area of that tile shape (fitted over the C3 sweep n = 28..300 on
+    // B200, profiles/r01_gemm_tile_sweep.txt: within 0.1 % of the per-size best)
     int T = 64;
     double best = 1e30;
-    for (int t : {64, 48, 32}) {
-      const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t);
+    const int tiles[6] = {64, 32, 56, 48, 72, 40};
+    const double wcost[6] = {1.000, 1.055, 1.102, 1.241, 1.300, 1.305};
+    for (int i = 0; i < 6; ++i) {
+      const int t = tiles[i];
+      const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t) * wcost[i];
       if (area < best * 0.999) best = area, T = t;
     }
+    static const int force_t = getenv("PB_GEMM_T") ? atoi(getenv("PB_GEMM_T")) : 0;  // tuning sweeps
+    if (force_t) T = force_t;
     const bool k40 = g.k > 32 && g.k <= 40;
     const bool cs = g.beta != 0.0 && g.tmaC;  // C tile through shared memory
-#define PB_TMA(T_, WM_, K_)                                                        \
-  if (T == T_ && (K_ == 40) == k40) {                                              \
-    if (cs) return launch_tma<T_, T_, WM_, 16, K_, (K_ == 40 ? 2 : 2), SYRK, 1>(g, st); \
-    return launch_tma<T_, T_, WM_, 16, K_, 3, SYRK, 0>(g, st);                     \
+#define PB_TMA(T_, WM_, WN_, K_)                                                     \
+  if (T == T_ && (K_ == 40) == k40) {                                                \
+    if (cs) return launch_tma<T_, T_, WM_, WN_, K_, 2, SYRK, 1>(g, st);              \
+    return launch_tma<T_, T_, WM_, WN_, K_, 3, SYRK, 0>(g, st);                      \
   }
-    PB_TMA(64, 32, 32) PB_TMA(64, 32, 40) PB_TMA(48, 24, 32) PB_TMA(48, 24, 40) PB_TMA(32, 16, 32) PB_TMA(32, 16, 40)
+    PB_TMA(64, 32, 16, 32) PB_TMA(64, 32, 16, 40) PB_TMA(48, 24, 16, 32) PB_TMA(48, 24, 16, 40)
+    PB_TMA(32, 16, 16, 32) PB_TMA(32, 16, 16, 40) PB_TMA(72, 24, 24, 32) PB_TMA(72, 24, 24, 40)
+    PB_TMA(56, 56, 8, 32) PB_TMA(56, 56, 8, 40) PB_TMA(40, 40, 8, 32) PB_TMA(40, 40, 8, 40)
 #undef PB_TMA
   }
   if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);
