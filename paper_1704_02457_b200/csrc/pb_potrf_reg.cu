@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
     // records its index and zeroes its reciprocal (the columns left of it
     // are final in a right-looking sweep and are never touched again; the
     // rest is garbage that the write mask drops).
+    //
+    // Within a panel the columns stay UNSCALED (u = L * sqrt(d)): the rank-1
+    // update uses  u[r][j] * u[c][j] / d_j  and the whole panel is scaled by
+    // its reciprocals once at the end (the diagonal u[c][c] is d_c itself, so
+    // u * (1/sqrt d) gives L[c][c] = sqrt(d_c) by the same rule).  The
+    // shuffles of column j then do not wait for its pivot's rsqrt.
 #pragma unroll
     for (int k = 0; k < GM; ++k) {
       double myinv = 0.0;
@@ -127,31 +133,30 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
         const bool bad = d <= 0.0;  // ccore.pyx:423 (NaN passes); warp-uniform
         if (bad && fail < 0) fail = 8 * k + j;
         const double inv = bad ? 0.0 : rsqrt_nr(d);
-        const double l = d * inv;
         if (lane == j) myinv = inv;
-        // scale column j (lanes q == h, element ej) by multipliers, so the
-        // update is one unconditional DMUL per tile (x1.0 elsewhere is exact)
-        const bool own = q == h;
-        const double sd = (own && r > j) ? inv : 1.0, so = own ? inv : 1.0;
-        {
-          const double v = T[ti(k, k)][ej] * sd;
-          T[ti(k, k)][ej] = (own && r == j) ? l : v;
-        }
-#pragma unroll
-        for (int i = k + 1; i < GM; ++i) T[ti(i, k)][ej] *= so;
         if (j < 7) {
-          // rank-1 update of the panel's columns c > j: the multiplier L[c][j]
-          // is zeroed in lanes whose column c <= j, so every update is one
+          // rank-1 update of the panel's columns c > j; the multiplier is
+          // zeroed in lanes whose column c <= j, so every update is one
           // unconditional FMA (the diagonal tile's strict upper is scratch)
           const double lc0 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + h);
           const double lc1 = __shfl_sync(FULL, T[ti(k, k)][ej], 8 * q + 4 + h);
-          const double m0 = 2 * q > j ? -lc0 : 0.0, m1 = 2 * q + 1 > j ? -lc1 : 0.0;
+          const double inv2 = inv * inv;
+          const double m0 = 2 * q > j ? -(lc0 * inv2) : 0.0, m1 = 2 * q + 1 > j ? -(lc1 * inv2) : 0.0;
 #pragma unroll
           for (int i = k; i < GM; ++i) {
-            const double prj = __shfl_sync(FULL, T[ti(i, k)][ej], 4 * r + h);  // P(i)[r][j]
+            const double prj = __shfl_sync(FULL, T[ti(i, k)][ej], 4 * r + h);  // u(i)[r][j]
             T[ti(i, k)][0] = fma(prj, m0, T[ti(i, k)][0]);
             T[ti(i, k)][1] = fma(prj, m1, T[ti(i, k)][1]);
           }
+        }
+      }
+      // scale the panel: column c = 2q + e by its reciprocal
+      {
+        const double s0 = __shfl_sync(FULL, myinv, 2 * q), s1 = __shfl_sync(FULL, myinv, 2 * q + 1);
+#pragma unroll
+        for (int i = k; i < GM; ++i) {
+          T[ti(i, k)][0] *= s0;
+          T[ti(i, k)][1] *= s1;
         }
       }
       // reciprocals of the completed columns (the reference writes dinv
