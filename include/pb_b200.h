@@ -19,6 +19,8 @@
  *   pb_dgemm_nn       <- ccore.gemm_nn_drv    (ccore.pyx:774-801)
  *   pb_dtrmm_rlnn     <- ccore.trmm_rlnn_drv  (ccore.pyx:834-852)
  *   pb_dsyrk_potrf_ln <- ccore.syrk_potrf_drv (ccore.pyx:908-941)
+ *   pb_dgetrf         <- level3._getrf / _getrf_inplace (level3.py:405-498) over
+ *                        kgetrf_panel, krowswap, lu_rowsolve_drv, gemm_nn_drv
  *
  * Conventions (mirroring the reference core):
  *   - caller owns every buffer; nothing here allocates device memory;
@@ -134,6 +136,18 @@ int pb_dsyrk_potrf_ln(int m, int n, int k,
                       const pb_dmat_batch *sC, int ci, int cj,
                       const pb_dmat_batch *sD, int di, int dj,
                       int32_t *info, void *stream);
+
+/* LU of the m x n window of C into D (level3.getrf_pivot / getrf_nopivot,
+ * level3.py:405-498): D holds unit-L below the diagonal and U on/above,
+ * diag_inv of D gets 1/U[j][j].  pivot != 0: partial pivoting, first
+ * largest |value| wins, ipiv[b*ipiv_stride + j] = row exchanged with j
+ * (completed 4-column panels only).  Bit-identical to the reference.
+ * info[b] = -1, or the first zero pivot; then D holds the partially
+ * factored window (panel-aligned di) or is untouched (di % 4 != 0), as the
+ * reference leaves it when it raises SingularMatrixError.
+ * Needs (m|1)*n*8 <= 220 KB (one item factored in shared memory). */
+int pb_dgetrf(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+              int pivot, int64_t *ipiv, int64_t ipiv_stride, int32_t *info, void *stream);
 
 /* Column-major -> panel-major copy (kpack_cm): item b's source element
  * (i, j) is S[b*s_stride + i + j*lds]. */

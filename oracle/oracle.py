@@ -49,6 +49,7 @@ def lib():
         _lib.po_memsize.restype = ctypes.c_int64
         _lib.po_potrf_l.restype = ctypes.c_int
         _lib.po_syrk_potrf_ln.restype = ctypes.c_int
+        _lib.po_getrf.restype = ctypes.c_int
     return _lib
 
 
@@ -258,6 +259,44 @@ def syrk_potrf_ln(m, k, A, ai, aj, B, bi, bj, C, ci, cj, D, di, dj, n=None):
     else:
         D.diag_lo = D.diag_hi = 0
     return info
+
+
+def getrf(m, n, C, ci, cj, D, di, dj, pivot, ipiv=None):
+    """level3._getrf semantics (level3.py:431-446) per item -> (info[batch], ipiv).
+
+    D = copy of C's window (skipped when D is C at the same origin), then the
+    in-place LU (po_getrf).  An unaligned destination (di % 4) is factored
+    in a scratch matrix and copied only on success (the reference raises
+    before its final gecp, so D stays untouched; diag_inv is written either
+    way).  ipiv[b, j0 + c] is filled for completed panels only."""
+    mn = min(m, n)
+    info = np.full(D.batch, -1, dtype=np.int32)
+    if ipiv is None:
+        ipiv = np.zeros((D.batch, max(mn, 1)), dtype=np.int64)
+    if mn == 0:
+        return info, ipiv
+    same = C is D and ci == di and cj == dj
+    for b in range(D.batch):
+        piv = np.ascontiguousarray(ipiv[b])
+        if di % 4 == 0:
+            if not same:
+                lib().po_gecp(_L(m), _L(n), _item(C, b), _L(ci), _L(cj), _L(C.cn), D.ptr(b), _L(di), _L(dj), _L(D.cn))
+            st = lib().po_getrf(_L(m), _L(n), ctypes.c_int(int(pivot)), D.ptr(b), _L(di), _L(dj), _L(D.cn),
+                                D.dptr(b), _L(dj), piv.ctypes.data_as(ctypes.c_void_p))
+        else:
+            s = HostBatch(1, m, n)
+            lib().po_gecp(_L(m), _L(n), _item(C, b), _L(ci), _L(cj), _L(C.cn), s.ptr(), _L(0), _L(0), _L(s.cn))
+            st = lib().po_getrf(_L(m), _L(n), ctypes.c_int(int(pivot)), s.ptr(), _L(0), _L(0), _L(s.cn),
+                                D.dptr(b), _L(dj), piv.ctypes.data_as(ctypes.c_void_p))
+            if st < 0:
+                lib().po_gecp(_L(m), _L(n), s.ptr(), _L(0), _L(0), _L(s.cn), D.ptr(b), _L(di), _L(dj), _L(D.cn))
+        ipiv[b] = piv
+        info[b] = st
+    if bool(np.all(info < 0)) and di == dj:
+        D.diag_lo, D.diag_hi = dj, dj + mn
+    else:
+        D.diag_lo = D.diag_hi = 0
+    return info, ipiv
 
 
 def pack_cm(m, n, S, lds, s_stride, D, di, dj):

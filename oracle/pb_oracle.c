@@ -306,6 +306,94 @@ int po_syrk_potrf_ln(ix m, ix n, ix k,
   return -1;
 }
 
+/* ---- §8f row 4: getrf (LU, with / without partial pivoting) ----------
+ * In place on D (the caller has copied C's window there), exactly
+ * level3._getrf_inplace (level3.py:448-498): left-looking 4-column panels;
+ * per panel the gemm_nn_drv downdate (ccore.pyx:774-801, store rule
+ * v = -1*acc + 1*C), kgetrf_panel (:563-650: pivot = first largest |.|,
+ * strict >, bv == 0 -> singular; row swap inside the panel's columns;
+ * inv = 1/u; column scaled by inv; rank-1 update skipped where u_cc == 0),
+ * then the deferred row swaps left/right of the panel (krowswap :661-670)
+ * and the U12 row solve (gemm_nn_drv + lu_rowsolve_drv :488-500 =
+ * _ktrsm_llnu_core :453-477 with km = 0: acc = 0.0 + 1.0*C, forward
+ * substitution with the unit-lower panel).  Returns -1 or the first zero
+ * pivot (global index); ipiv[j0 + c] = j0 + r only for completed panels;
+ * dinv[dio + c] for completed columns. */
+int po_getrf(ix m, ix n, int pivot, double *D, ix di, ix dj, ix sdd, double *dinv, ix dio, int64_t *ipiv) {
+  const ix mn = m < n ? m : n;
+#define E(i, j) D[eo(di + (i), dj + (j), sdd)]
+  for (ix j0 = 0; j0 < mn; j0 += 4) {
+    const ix jb = mn - j0 < 4 ? mn - j0 : 4;
+    if (j0 > 0)
+      po_gemm_nn(m - j0, jb, j0, -1.0, D, di + j0, dj, sdd, D, di, dj + j0, sdd, 1.0, D, di + j0, dj + j0, sdd, D,
+                 di + j0, dj + j0, sdd);
+    ix piv[4] = {0, 0, 0, 0};
+    for (ix c = 0; c < jb; ++c) {
+      const ix gc = j0 + c;
+      if (pivot) {
+        ix best = c;
+        double bv = fabs(E(gc, gc));
+        for (ix r = c + 1; r < m - j0; ++r) {
+          const double v = fabs(E(j0 + r, gc));
+          if (v > bv) bv = v, best = r;
+        }
+        if (bv == 0.0) return (int)gc;
+        piv[c] = best;
+        if (best != c)
+          for (ix cc = 0; cc < jb; ++cc) {
+            const double t = E(gc, j0 + cc);
+            E(gc, j0 + cc) = E(j0 + best, j0 + cc);
+            E(j0 + best, j0 + cc) = t;
+          }
+      } else if (E(gc, gc) == 0.0) {
+        return (int)gc;
+      }
+      const double u = E(gc, gc);
+      const double inv = 1.0 / u;
+      dinv[dio + gc] = inv;
+      for (ix r = gc + 1; r < m; ++r) E(r, gc) *= inv;
+      for (ix cc = c + 1; cc < jb; ++cc) {
+        const double ucc = E(gc, j0 + cc);
+        if (ucc != 0.0)
+          for (ix r = gc + 1; r < m; ++r) E(r, j0 + cc) -= E(r, gc) * ucc;
+      }
+    }
+    if (pivot)
+      for (ix cc = 0; cc < jb; ++cc) {
+        const ix r = piv[cc];
+        ipiv[j0 + cc] = j0 + r;
+        if (r != cc) {
+          for (ix j = 0; j < j0; ++j) {
+            const double t = E(j0 + cc, j);
+            E(j0 + cc, j) = E(j0 + r, j);
+            E(j0 + r, j) = t;
+          }
+          for (ix j = j0 + jb; j < n; ++j) {
+            const double t = E(j0 + cc, j);
+            E(j0 + cc, j) = E(j0 + r, j);
+            E(j0 + r, j) = t;
+          }
+        }
+      }
+    if (j0 + jb < n) {
+      if (j0 > 0)
+        po_gemm_nn(jb, n - j0 - jb, j0, -1.0, D, di + j0, dj, sdd, D, di, dj + j0 + jb, sdd, 1.0, D, di + j0,
+                   dj + j0 + jb, sdd, D, di + j0, dj + j0 + jb, sdd);
+      for (ix j = j0 + jb; j < n; ++j) {
+        double acc[4];
+        for (ix i = 0; i < jb; ++i) acc[i] = 0.0 + 1.0 * E(j0 + i, j);
+        for (ix i = 0; i < jb; ++i) {
+          const double x = acc[i];
+          for (ix t = i + 1; t < jb; ++t) acc[t] -= E(j0 + t, j0 + i) * x;
+        }
+        for (ix i = 0; i < jb; ++i) E(j0 + i, j) = acc[i];
+      }
+    }
+  }
+#undef E
+  return -1;
+}
+
 /* ---- naive column-major oracles: ccore.pyx:1109-1223 (o_*) ----
  * Independent of the panel machinery; used to cross-check the above. */
 void po_naive_potrf(ix m, const double *C, ix ldc, double *L, ix ldl) {

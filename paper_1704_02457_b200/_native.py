@@ -52,6 +52,7 @@ SIGNATURES = {
     "pb_dtrmm_rlnn": (_i, [_i, _i, _d, P, _i, _i, P, _i, _i, P, _i, _i, _v]),
     "pb_dsyrk_potrf_ln": (_i, [_i, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, _v, _v]),
     "pb_driccati_chain": (_i, [_i, _i, _i, P, P, P, P, _v, _v]),
+    "pb_dgetrf": (_i, [_i, _i, P, _i, _i, P, _i, _i, _i, _v, _l, _v, _v]),
 }
 
 

@@ -76,6 +76,27 @@ extern "C" {
 
 int pb_version(void) { return 1; }
 const char *pb_last_error(void) { return t_err.c_str(); }
+int pb_dgetrf(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+              int pivot, int64_t *ipiv, int64_t ipiv_stride, int32_t *info, void *stream) {
+  // positions: m1 n2 C3 ci4 cj5 D6 di7 dj8 pivot9 ipiv10 ipiv_stride11 info12 (level3.py:405-446)
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0) return fail_arg(2, "negative size");
+  if (!sD) return fail_arg(6, "null matrix descriptor");
+  const int batch = sD->batch;
+  int r;
+  if ((r = check_mat(sC, 3, ci, cj, m, n, batch, false))) return r;
+  if ((r = check_mat(sD, 6, di, dj, m, n, batch, true))) return r;
+  const int mn = m < n ? m : n;
+  if (mn == 0 || batch == 0) return 0;  // level3.py:435-436
+  if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
+  if (pivot && !ipiv) return fail_arg(10, "ipiv is required with pivoting");
+  if (pivot && ipiv_stride < mn) return fail_arg(11, "ipiv stride below min(m, n)");
+  if (!info) return fail_arg(12, "info is required");
+  if (getrf_smem(m, n) > 220 * 1024) return fail_arg(1, "window too large for the shared-memory LU (m*n*8 > 220 KB)");
+  return finish(run_getrf(m, n, pivot ? 1 : 0, to_mat(sC), ci, cj, to_mat(sD), di, dj, ipiv, ipiv_stride, info, batch,
+                          (cudaStream_t)stream));
+}
+
 int64_t pb_launch_count(int reset) {
   const int64_t v = t_launches;
   if (reset) t_launches = 0;

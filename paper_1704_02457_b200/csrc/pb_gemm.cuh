@@ -78,5 +78,8 @@ bool potrf_reg_ok(const PotrfArgs &g);
 cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
+size_t getrf_smem(int m, int n);
+cudaError_t run_getrf(int m, int n, int pivot, const Mat &C, ix ci, ix cj, const Mat &D, ix di, ix dj, int64_t *ipiv,
+                      ix ipiv_stride, int32_t *info, ix batch, cudaStream_t st);
 
 }  // namespace pb

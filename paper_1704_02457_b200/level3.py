@@ -284,3 +284,59 @@ def syrk_potrf_ln(m, k, A, B, C, D, n=None, check=True):
                 batch_index=f[0], info=info)
     _mark_diag(d, dj, n, di == dj)
     return info
+
+
+# ---------------------------------------------------------------------------
+# LU
+
+
+def _getrf(m, n, C, D, pivot, ipiv, check, name):
+    # level3.py:431-446: bounds, min(m, n) == 0 no-op, D <- C window, in-place LU
+    c, ci, cj = _ref(C, "C")
+    d, di, dj = _ref(D, "D")
+    _check(c, ci, cj, m, n, "C")
+    _check(d, di, dj, m, n, "D")
+    nb = _batch_of(d, c)
+    mn = min(m, n)
+    if mn == 0 or nb == 0:
+        return None
+    if pivot:
+        if ipiv is None:
+            ipiv = torch.zeros((nb, mn), dtype=torch.int64, device=d.device)
+        elif ipiv.dim() != 2 or ipiv.shape[0] != nb or ipiv.shape[1] < mn or ipiv.dtype != torch.int64 \
+                or ipiv.device != d.device or ipiv.stride(1) != 1:
+            raise DimensionError(f"ipiv needs shape ({nb}, >= {mn}) int64 on {d.device}, unit column stride")
+    info = torch.empty(nb, dtype=torch.int32, device=d.device)
+    dc, dd = c.descriptor(nb), d.descriptor(nb)
+    _native.call("pb_dgetrf", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, 1 if pivot else 0,
+                 ctypes.c_void_p(ipiv.data_ptr() if pivot else 0), ipiv.stride(0) if pivot else 0,
+                 ctypes.c_void_p(info.data_ptr()), _stream(d.device))
+    if check:
+        f = _first_failure(info)
+        if f is not None:
+            _mark_diag(d, dj, 0, False)
+            raise SingularMatrixError(f"{name}: zero pivot at index {f[1]} (batch item {f[0]})", f[1],
+                                      batch_index=f[0], info=info)
+    _mark_diag(d, dj, mn, di == dj)
+    return ipiv if pivot else info
+
+
+def getrf_nopivot(m, n, C, D, check=True):
+    """LU without pivoting of every item (level3.py:405-411): D holds unit-L
+    below the diagonal and U on/above, D.diag_inv the reciprocals of U's
+    diagonal.  Bit-identical to the reference.  Returns ``info``; with
+    ``check`` an exactly-zero pivot raises SingularMatrixError (index, and
+    the batch_index of the first failing item)."""
+    return _getrf(m, n, C, D, False, None, check, "getrf_nopivot")
+
+
+def getrf_pivot(m, n, C, D, ipiv=None, check=True):
+    """LU with partial pivoting, P*C = L*U, of every item (level3.py:414-428).
+
+    ``ipiv`` is an int64 tensor (batch, >= min(m, n)) of transpositions:
+    ipiv[b, j] = r means rows j and r (r >= j) were exchanged at step j;
+    allocated when not supplied and returned either way.  The pivot is the
+    largest magnitude, ties toward the lowest row (bit-identical to the
+    reference, so ipiv matches exactly)."""
+    return _getrf(m, n, C, D, True, ipiv, check, "getrf_pivot")
+

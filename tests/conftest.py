@@ -31,8 +31,8 @@ def rel(a, b):
     return float(np.max(np.abs(a - b))) / max(1.0, float(np.max(np.abs(b))))
 
 
-def load_golden():
-    z = np.load(GOLDEN)
+def load_golden(name=None):
+    z = np.load(GOLDEN if name is None else os.path.join(os.path.dirname(GOLDEN), name))
     manifest = json.loads(str(z["manifest"]))
     return z, manifest["cases"]
 

@@ -3,7 +3,8 @@
 Run in the build container (where /root/reference exists):
 
     make -C oracle ref                 # cythonize + compile the reference's own ccore
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # golden_v1.npz
+    python tests/golden/make_golden.py --getrf    # golden_getrf_v1.npz (§8f getrf)
 
 It imports the reference package ``panelblas`` read-only from
 /root/reference/pkg/src with its compiled core from oracle/_ref (or, if
@@ -293,6 +294,27 @@ def pack_case(name, rng, m, n, od):
            lambda: pack.pack_matrix(ColMatrix.from_array(arr), m, n, D.ref(*od)) if m * n else None)
 
 
+def getrf_case(name, rng, m, n, pivot, oc=(0, 0), od=(0, 0), c=None, in_place=False, dfill=0.0):
+    """level3.getrf_pivot / getrf_nopivot (level3.py:405-498); ipiv recorded too."""
+    c = rng.uniform(-1, 1, (m, n)) if c is None else np.asarray(c, dtype=np.float64)
+    C = zmat(oc[0] + m + 1, oc[1] + n + 2)
+    put(C, *oc, c)
+    if in_place:
+        D, od = C, oc
+    else:
+        D = zmat(od[0] + m + 2, od[1] + n + 1, fill=dfill)
+    mn = min(m, n)
+    ipiv = np.full(max(mn, 1), -7, dtype=np.int64)
+    p = dict(m=m, n=n, pivot=int(pivot), ci=oc[0], cj=oc[1], di=od[0], dj=od[1])
+    key = f"c{len(CASES):03d}"
+    if pivot:
+        fn = lambda: level3.getrf_pivot(m, n, C.ref(*oc), D.ref(*od), ipiv=ipiv[:mn] if mn else ipiv)  # noqa: E731
+    else:
+        fn = lambda: level3.getrf_nopivot(m, n, C.ref(*oc), D.ref(*od))  # noqa: E731
+    record(name, "getrf", p, {"C": C, "D": D}, fn)
+    ARRAYS[f"{key}/ipiv"] = ipiv.copy()
+
+
 def main():
     rng = np.random.default_rng(20261020)
     # ---- gemm_nt
@@ -403,5 +425,36 @@ def main():
     print(f"wrote {len(CASES)} cases to {out} (reference backend {pb.backend_name()})")
 
 
+def main_getrf():
+    """tests/golden/golden_getrf_v1.npz: the §8f getrf cases (separate file, own seed)."""
+    rng = np.random.default_rng(20261021)
+    getrf_case("getrf_identity", rng, 5, 5, True, c=np.eye(5))
+    getrf_case("getrf_forced_swap", rng, 2, 2, True, c=np.array([[0.0, 1.0], [2.0, 3.0]]))
+    for m, n in [(4, 4), (7, 7), (9, 9), (12, 12), (16, 16), (5, 11), (13, 6), (24, 24), (33, 33), (40, 17)]:
+        getrf_case(f"getrf_pivot_{m}x{n}", rng, m, n, True)
+        getrf_case(f"getrf_nopivot_{m}x{n}", rng, m, n, False, c=rng.uniform(-1, 1, (m, n)) + 4.0 * np.eye(m, n))
+    getrf_case("getrf_pivot_ties", rng, 8, 8, True, c=np.round(rng.uniform(-2, 2, (8, 8))))
+    getrf_case("getrf_pivot_unaligned", rng, 10, 9, True, oc=(3, 2), od=(1, 3), dfill=2.5)
+    getrf_case("getrf_pivot_aligned_off", rng, 9, 10, True, oc=(1, 1), od=(4, 2), dfill=2.5)
+    getrf_case("getrf_in_place", rng, 11, 11, True, in_place=True)
+    cz = rng.uniform(-1, 1, (6, 6))
+    cz[:, 3] = 0.0
+    getrf_case("getrf_pivot_zero_column", rng, 6, 6, True, c=cz, dfill=2.5)
+    cn = rng.uniform(-1, 1, (5, 5)) + 3 * np.eye(5)
+    cn[2, 2] = 0.0
+    cn[2, :2] = 0.0
+    cn[:2, 2] = 0.0
+    getrf_case("getrf_nopivot_zero_pivot", rng, 5, 5, False, c=cn, dfill=2.5)
+    getrf_case("getrf_pivot_zero_column_unaligned", rng, 6, 6, True, c=cz, od=(2, 1), dfill=2.5)
+
+    out = os.path.join(HERE, "golden_getrf_v1.npz")
+    ARRAYS["manifest"] = np.array(json.dumps({"backend": pb.backend_name(), "cases": CASES}))
+    np.savez_compressed(out, **ARRAYS)
+    print(f"wrote {len(CASES)} cases to {out} (reference backend {pb.backend_name()})")
+
+
 if __name__ == "__main__":
-    main()
+    if "--getrf" in sys.argv:
+        main_getrf()
+    else:
+        main()

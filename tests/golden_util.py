@@ -51,6 +51,12 @@ def run_oracle(case, mats, z=None):
         info = O.syrk_potrf_ln(p["m"], p["k"], mats["A"], p["ai"], p["aj"], mats["B"], p["bi"], p["bj"],
                                mats["C"], p["ci"], p["cj"], mats["D"], p["di"], p["dj"], n=p["n"])
         return int(info[0])
+    if op == "getrf":
+        ipiv = np.full((mats["D"].batch, max(min(p["m"], p["n"]), 1)), -7, dtype=np.int64)
+        info, ipiv = O.getrf(p["m"], p["n"], mats["C"], p["ci"], p["cj"], mats["D"], p["di"], p["dj"], p["pivot"],
+                             ipiv=ipiv)
+        mats["_ipiv"] = ipiv
+        return int(info[0])
     if op == "pack":
         m, n = p["m"], p["n"]
         if m * n:

@@ -91,6 +91,18 @@ def run_product(case, mats):
         return level3.syrk_potrf_ln(p["m"], p["k"], mats["A"].ref(p["ai"], p["aj"]), mats["B"].ref(p["bi"], p["bj"]),
                                     mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]), n=p["n"],
                                     check=False)
+    if op == "getrf":
+        nb = mats["D"].batch
+        mn = max(min(p["m"], p["n"]), 1)
+        ipiv = torch.full((nb, mn), -7, dtype=torch.int64, device="cuda")
+        fn = level3.getrf_pivot if p["pivot"] else level3.getrf_nopivot
+        args = (p["m"], p["n"], mats["C"].ref(p["ci"], p["cj"]), mats["D"].ref(p["di"], p["dj"]))
+        if p["pivot"]:
+            fn(*args, ipiv=ipiv, check=False)
+        else:
+            fn(*args, check=False)
+        mats["_ipiv"] = ipiv
+        return None
     raise ValueError(op)
 
 
@@ -523,6 +535,116 @@ def test_potrf_small_in_place_and_offset_bit_exact(n):
     winfo = O.potrf_l(n, C2, 0, 0, D, 4, 3)
     assert np.array_equal(info, winfo)
     assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64))
+
+
+@pytest.mark.parametrize("batch", [1, 6])
+def test_getrf_golden_bit_exact(batch):
+    """§8f getrf against the reference's own recorded outputs: storage
+    (partial state of failing items included), ipiv and diag validity, bit
+    for bit, replicated over a batch."""
+    z, cases = load_golden("golden_getrf_v1.npz")
+    for case in cases:
+        hm = host_inputs(z, case, batch)
+        dm = {}
+        for lab, h in hm.items():
+            if lab not in case["alias"]:
+                dm[lab] = dev(h)
+        for lab, tgt in case["alias"].items():
+            dm[lab] = dm[tgt]
+        dD = dm[case["alias"].get("D", "D")]
+        nb = dD.batch
+        p = case["params"]
+        mn = max(min(p["m"], p["n"]), 1)
+        ipiv = torch.full((nb, mn), -7, dtype=torch.int64, device="cuda")
+        fn = level3.getrf_pivot if p["pivot"] else level3.getrf_nopivot
+        args = (p["m"], p["n"], dm["C"].ref(p["ci"], p["cj"]), dD.ref(p["di"], p["dj"]))
+        if case["status"] >= 0:
+            with pytest.raises(pb.SingularMatrixError) as ei:
+                fn(*args, ipiv=ipiv) if p["pivot"] else fn(*args)
+            assert ei.value.index == case["status"] and ei.value.batch_index == 0, case["name"]
+        else:
+            fn(*args, ipiv=ipiv) if p["pivot"] else fn(*args)
+        for lab in out_labels(case):
+            want = z[f"{case['key']}/out/{lab}"]
+            got = host(dm[lab])[:, : want.size]
+            for b in range(batch):
+                assert np.array_equal(got[b].view(np.uint64), want.view(np.uint64)), (case["name"], lab, b)
+        if p["pivot"]:
+            want_piv = z[f"{case['key']}/ipiv"]
+            got_piv = ipiv.cpu().numpy()
+            for b in range(batch):
+                assert np.array_equal(got_piv[b, : want_piv.size], want_piv), (case["name"], b)
+        assert [dD.diag_lo, dD.diag_hi] == case["valid_out"]["D"], case["name"]
+
+
+@pytest.mark.parametrize("mn", [(4, 4), (9, 9), (16, 16), (23, 17), (17, 30), (32, 32), (48, 48), (64, 64), (100, 60)])
+def test_getrf_random_vs_oracle_bit_exact(mn):
+    """Random batches (pivot and no pivot), window offsets, in place, and a
+    few singular items: storage, info and ipiv equal the oracle's bit for bit."""
+    m, n = mn
+    rng = np.random.default_rng(31 * m + n)
+    nb = 37
+    for pivot in (True, False):
+        for (oc, od) in [((0, 0), (0, 0)), ((3, 2), (4, 1)), ((1, 0), (2, 3))]:
+            a = rng.uniform(-1, 1, (nb, m, n))
+            if not pivot:
+                a += 4.0 * np.eye(m, n)
+            for b in range(2, nb, 9):
+                a[b, :, min(m, n) // 2] = 0.0  # singular column
+            C = rand_batch(rng, nb, oc[0] + m + 1, oc[1] + n + 2)
+            C.set_window(oc[0], oc[1], a)
+            D = rand_batch(rng, nb, od[0] + m + 2, od[1] + n + 1)
+            dC, dD = dev(C), dev(D)
+            k = min(m, n)
+            ipiv = torch.full((nb, k), -7, dtype=torch.int64, device="cuda")
+            if pivot:
+                level3.getrf_pivot(m, n, dC.ref(*oc), dD.ref(*od), ipiv=ipiv, check=False)
+            else:
+                info = level3.getrf_nopivot(m, n, dC.ref(*oc), dD.ref(*od), check=False)
+            wpiv = np.full((nb, k), -7, dtype=np.int64)
+            winfo, wpiv = O.getrf(m, n, C, *oc, D, *od, pivot, ipiv=wpiv)
+            assert np.array_equal(host(dD).view(np.uint64), D.storage.view(np.uint64)), (mn, pivot, oc, od)
+            if pivot:
+                assert np.array_equal(ipiv.cpu().numpy(), wpiv), (mn, oc, od)
+            else:
+                assert np.array_equal(info.cpu().numpy(), winfo), (mn, oc, od)
+    # in place (D == C)
+    a = rng.uniform(-1, 1, (nb, m, n))
+    C = rand_batch(rng, nb, m, n)
+    C.set_window(0, 0, a)
+    dC = dev(C)
+    ipiv = torch.zeros((nb, min(m, n)), dtype=torch.int64, device="cuda")
+    level3.getrf_pivot(m, n, dC, dC, ipiv=ipiv, check=False)
+    _, wpiv = O.getrf(m, n, C, 0, 0, C, 0, 0, True)
+    assert np.array_equal(host(dC).view(np.uint64), C.storage.view(np.uint64))
+    assert np.array_equal(ipiv.cpu().numpy(), wpiv)
+
+
+def test_getrf_reconstruction_and_edge_rules():
+    """P*C = L*U to rounding; m or n == 0 is a no-op; a window too large for
+    the shared-memory LU is refused before any launch."""
+    rng = np.random.default_rng(5)
+    nb, m = 8, 20
+    a = rng.uniform(-1, 1, (nb, m, m))
+    C = pack.panel_from_array(a)
+    D = pb.allocate_panel_batch(nb, m, m, zero=True)
+    ipiv = level3.getrf_pivot(m, m, C, D)
+    lu = pack.panel_to_array(D).cpu().numpy()
+    piv = ipiv.cpu().numpy()
+    for b in range(nb):
+        lo = np.tril(lu[b], -1) + np.eye(m)
+        up = np.triu(lu[b])
+        pc = a[b].copy()
+        for j in range(m):
+            pc[[j, piv[b, j]]] = pc[[piv[b, j], j]]
+        assert np.linalg.norm(lo @ up - pc) <= 1e-12 * np.linalg.norm(a[b])
+        assert np.max(np.abs(D.diag_inv[b].cpu().numpy() * np.diag(up) - 1.0)) <= 1e-15
+    before = D.storage.clone()
+    assert level3.getrf_pivot(0, m, C, D) is None and level3.getrf_nopivot(m, 0, C, D) is None
+    assert torch.equal(before, D.storage)
+    big = pb.allocate_panel_batch(1, 200, 200, zero=True)
+    with pytest.raises(RuntimeError):
+        level3.getrf_pivot(200, 200, big, big)
 
 
 def test_riccati_chain_c5_vs_oracle_and_graph_replay():

@@ -97,7 +97,7 @@ def _header_symbols():
 def test_native_library_exports_header_surface():
     lib = _native.load()
     syms = _header_symbols()
-    assert len(syms) == 16, syms
+    assert len(syms) == 17, syms
     assert set(syms) == set(_native.SIGNATURES)
     for s in syms:
         assert hasattr(lib, s), s
@@ -110,6 +110,8 @@ def test_native_library_exports_header_surface():
     assert lib.pb_dpotrf_l(4, 5, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, None, None) == -2
     assert lib.pb_dgemm_nt(4, 4, 4, 1.0, ctypes.byref(d), 1, 0, ctypes.byref(d), 0, 0, 0.0, ctypes.byref(d), 0, 0,
                            ctypes.byref(d), 0, 0, None) == -5
+    assert lib.pb_dgetrf(4, 4, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, 1, None, 4, None, None) == -10
+    assert b"ipiv" in lib.pb_last_error()
     assert lib.pb_launch_count(0) == 0
 
 

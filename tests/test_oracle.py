@@ -45,6 +45,26 @@ def test_golden_cases_bit_exact():
             assert [d.diag_lo, d.diag_hi] == case["valid_out"]["D"], case["name"]
 
 
+def test_golden_getrf_bit_exact():
+    """§8f getrf (level3.py:405-498): storage, status, ipiv and diag validity
+    bit-exact against the reference's own outputs."""
+    z, cases = load_golden("golden_getrf_v1.npz")
+    assert len(cases) >= 25
+    for case in cases:
+        mats = host_inputs(z, case)
+        st = run_oracle(case, mats, z)
+        assert st == case["status"], (case["name"], st, case["status"])
+        for lab in out_labels(case):
+            want = z[f"{case['key']}/out/{lab}"]
+            got = mats[lab].storage[0, : want.size]
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (case["name"], lab)
+        want_piv = z[f"{case['key']}/ipiv"]
+        if case["params"]["pivot"]:
+            assert np.array_equal(mats["_ipiv"][0][: want_piv.size], want_piv), case["name"]
+        d = mats[case["alias"].get("D", "D")]
+        assert [d.diag_lo, d.diag_hi] == case["valid_out"]["D"], case["name"]
+
+
 def _load_ref_core():
     so = glob.glob(os.path.join(REPO, "oracle", "_ref", "ccore*.so"))
     if not so:
