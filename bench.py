@@ -96,6 +96,10 @@ class Point:
             self.flops_item = float(m) * (m + 1) * k + m ** 3 / 3.0
             self.bytes_item = 8.0 * (m * k + m * (m + 1) + m)
             self.io_bytes = memsize(m, k) + 2 * memsize(m, m)
+        elif op == "getrf":  # getrf_pivot, square; reference flop_count 2m^3/3 (bench.py:97-98)
+            self.flops_item = 2.0 * m ** 3 / 3.0
+            self.bytes_item = 8.0 * (2 * m * n + min(m, n)) + 8.0 * min(m, n)  # C in, D + diag_inv + ipiv out
+            self.io_bytes = 2 * memsize(m, n) + 8 * min(m, n)
         elif op == "riccati_fact":  # apps.riccati_factorize: m = nx, n = nu, k = N; bench.py:98-101
             nx, nu, ns = m, n, m + n
             self.flops_item = k * (float(ns) * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0)
@@ -121,6 +125,8 @@ class Point:
             return f"riccati_factorize nx={self.m} nu={self.n} N={self.k}"
         if self.op in ("gemm_nn", "syrk_potrf_ln"):
             return f"{self.op} {self.m}x{self.n}x{self.k}"
+        if self.op == "getrf":
+            return f"getrf_pivot {self.m}x{self.n}"
         if self.op == "riccati":
             return f"riccati nx={self.m} nu={self.n} N={self.k}"
         if self.op == "potrf_l":
@@ -152,9 +158,10 @@ def config_points(name):
             "C5 Riccati-style chain: 1024 problems x N=50 stages, nx=32 nu=8 (gemm_nt, syrk_ln, potrf_l, trsm_rltn, gemm_nt per stage)"
     if name == "c6":
         return [Point("gemm_nn", 64, 64, 64, 4096, 1.0, 1.0), Point("trmm_rlnn", 40, 32, 0, 16384, 1.0),
-                Point("syrk_potrf_ln", 40, 40, 32, 16384), Point("riccati_fact", 32, 8, 50, 1024)], \
+                Point("syrk_potrf_ln", 40, 40, 32, 16384), Point("riccati_fact", 32, 8, 50, 1024),
+                Point("getrf", 32, 32, 0, 16384)], \
             ("C6 next tier (SURVEY §8f): dgemm_nn 64^3 batch 4096, dtrmm_rlnn 40x32 and dsyrk_potrf_ln 40x40 k=32 "
-             "batch 16384, apps.riccati_factorize nx=32 nu=8 N=50 x 1024 problems")
+             "batch 16384, apps.riccati_factorize nx=32 nu=8 N=50 x 1024 problems, dgetrf_pivot 32x32 batch 16384")
     raise SystemExit(f"unknown config {name}")
 
 
@@ -253,6 +260,11 @@ class GpuPoint:
             pack.pack_array_into(torch.baddbmm(torch.eye(m, dtype=torch.float64, device=device).expand(nb, m, m) * m,
                                                Md, Md.transpose(1, 2)), self.C)
             self.D = pb.allocate_panel_batch(nb, m, m, device=device, zero=True)
+        elif pt.op == "getrf":
+            self.C = pb.allocate_panel_batch(nb, m, n, device=device)
+            self.C.storage.uniform_(-1, 1, generator=g)
+            self.D = pb.allocate_panel_batch(nb, m, n, device=device, zero=True)
+            self.ipiv = torch.zeros((nb, min(m, n)), dtype=torch.int64, device=device)
         elif pt.op == "riccati_fact":
             from paper_1704_02457_b200 import composite
             nx, nu, N = m, n, k
@@ -319,6 +331,8 @@ class GpuPoint:
                 level3.trmm_rlnn(pt.m, pt.n, pt.alpha, self.A, self.B, self.D)
             elif pt.op == "syrk_potrf_ln":
                 level3.syrk_potrf_ln(pt.m, pt.k, self.A, self.A, self.C, self.D, check=False)
+            elif pt.op == "getrf":
+                level3.getrf_pivot(pt.m, pt.n, self.C, self.D, ipiv=self.ipiv, check=False)
             elif pt.op == "riccati_fact":
                 self.graph.replay()  # whole backward sweep: one graph of trmm + syrk/gemm + potrf per stage
                 GRAPH_LAUNCHES[0] += self.graph_kernels
@@ -670,6 +684,39 @@ def _cpu_worker(job):
                 core.gemm_nt_drv(nx, nx, nx, 1.0, F, nu, nu, sds, F, nu, nu, sds, 0.0, P, 0, 0, sdx, P, 0, 0, sdx)
         flops_item = N * (2.0 * ns * nx * nx + float(ns) * (ns + 1) * nx + ns ** 3 / 3.0 + float(nx) * nu * nu
                           + 2.0 * nx * nx * nx)
+        Cs = [None]
+    elif op == "getrf":
+        # level3._getrf_inplace (level3.py:448-498) over the reference's own core
+        sd = ru(n)
+        src = rng.uniform(-1, 1, ru(m) * sd)
+        Dm = np.zeros_like(src)
+        dv = np.zeros(min(m, n))
+        sp = np.zeros(4, dtype=np.int64)
+        mn = min(m, n)
+
+        def call(c):
+            Dm[:] = src
+            for j0 in range(0, mn, 4):
+                jb = min(4, mn - j0)
+                if j0 > 0:
+                    core.gemm_nn_drv(m - j0, jb, j0, -1.0, Dm, j0, 0, sd, Dm, 0, j0, sd, 1.0, Dm, j0, j0, sd,
+                                     Dm, j0, j0, sd)
+                core.kgetrf_panel(Dm, j0 * sd + 4 * j0, sd, m - j0, jb, True, sp, 0, dv, j0)
+                for cc in range(jb):
+                    r = int(sp[cc])
+                    if r != cc:
+                        o1 = ((j0 + cc) & ~3) * sd + ((j0 + cc) & 3)
+                        o2 = ((j0 + r) & ~3) * sd + ((j0 + r) & 3)
+                        if j0 > 0:
+                            core.krowswap(j0, Dm, o1, Dm, o2)
+                        if j0 + jb < n:
+                            core.krowswap(n - j0 - jb, Dm, o1 + 4 * (j0 + jb), Dm, o2 + 4 * (j0 + jb))
+                if j0 + jb < n:
+                    if j0 > 0:
+                        core.gemm_nn_drv(jb, n - j0 - jb, j0, -1.0, Dm, j0, 0, sd, Dm, 0, j0 + jb, sd, 1.0,
+                                         Dm, j0, j0 + jb, sd, Dm, j0, j0 + jb, sd)
+                    core.lu_rowsolve_drv(jb, n - j0 - jb, Dm, j0, j0, j0 + jb, sd)
+        flops_item = 2.0 * m ** 3 / 3.0
         Cs = [None]
     elif op == "riccati_fact":
         nx, nu, N = m, n, k
