@@ -477,6 +477,12 @@ def run_ours(args):
                     "frac": dp["gflops"] / world / FP64_PEAK_GFLOPS, "peak_src": FP64_PEAK_SRC}
     roofline.update({"kernel": dp["point"], "share_of_step": dp["ms"] / step_ms,
                      "traffic": traffic_from_profile(dpt), "per_launch_ms": dp["ms"] / dpt.reps})
+    if roofline["traffic"]:
+        # measured DRAM bytes (ncu) over this run's launch time: how close the kernel runs to
+        # peak DRAM throughput for the traffic the layout and write set force on it
+        dram = roofline["traffic"] / (roofline["per_launch_ms"] * 1e-3) / 1e9  # per GPU
+        roofline.update({"dram_gbs": dram, "dram_frac": dram / HBM_GBS,
+                         "traffic_alg_ratio": roofline["traffic"] / (dpt.bytes_item * dpt.chunk)})
 
     e2e = run_e2e(args, gps, device, world, rank) if not args.no_e2e else None
     cpu = None
