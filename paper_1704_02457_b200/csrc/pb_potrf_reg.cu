@@ -65,7 +65,12 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
   // one warp per CTA: the item index is CTA-uniform, so the compiler sees
   // converged control flow around every shuffle and DMMA
   const ix nw = (ix)gridDim.x;
-  const unsigned pf_bytes = 32u * (unsigned)g.C.cn * (unsigned)((n + 3) / 4);
+  // L2 prefetch of the next item (PB_REG_PF): 1 = one bulk prefetch of its
+  // whole panels (default, measured best), 2 = only each panel's lower
+  // prefix, one prefetch per lane (fewer bytes, measured 2-3 % slower),
+  // 0 = none (10-20 % slower); prefetching D too was 25 % slower
+  const int np4 = (n + 3) / 4;
+  const unsigned pf_bytes = 32u * (unsigned)min(4 * lane + 4, n);
   // per-lane row offsets of the window rows 8i + r (panel carry included),
   // so an element address is one add of a compile-time column offset
   ix offC[GM], offD[GM];
@@ -76,8 +81,10 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
   }
   for (ix b = (ix)blockIdx.x; b < g.batch; b += nw) {
     const double *Cb = g.C.p + b * g.C.stride;
-    if (pf_ok && lane == 0 && b + nw < g.batch)
-      prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci, 0, g.C.cn), pf_bytes);
+    if (pf_ok == 2 && lane < np4 && b + nw < g.batch)
+      prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci + 4 * lane, g.cj, g.C.cn), pf_bytes);
+    if (pf_ok == 1 && lane == 0 && b + nw < g.batch)
+      prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci, 0, g.C.cn), 32u * (unsigned)g.C.cn * (unsigned)np4);
     double T[NT][2];
 #pragma unroll
     for (int i = 0; i < GM; ++i)
@@ -219,7 +226,8 @@ cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
   ix grid = (ix)num_sms() * occ;
   if (grid > ctas) grid = ctas;
   if (grid < 1) grid = 1;
-  const int pf_ok = (g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0;
+  static const int pf_mode = getenv("PB_REG_PF") ? atoi(getenv("PB_REG_PF")) : 1;  // A/B: 0 none, 1 panels, 2 prefixes
+  const int pf_ok = ((g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0) ? pf_mode : 0;
   kern<<<(unsigned)grid, 32, 0, st>>>(g, pf_ok);
   note_launch();
   return cudaGetLastError();
