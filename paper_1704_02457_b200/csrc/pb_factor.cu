@@ -674,11 +674,27 @@ cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *
 }
 
 cudaError_t run_trsm_rltn(const TrsmArgs &g, cudaStream_t st) {
+  // team width: the warps of a team take the item's 8-row strips round-robin
+  // and meet at a barrier per item, so pick the width with the best strip
+  // utilisation gmr / (TW * rounds) (ties -> wider team, fewer rounds): e.g.
+  // C4's m = 72 (9 strips) runs 3 rounds on 3 warps instead of 2 on 8
   const ix gmr = (g.m + 7) / 8;
-  if (gmr <= 1) return launch_trsm<1>(g, st);
-  if (gmr <= 2) return launch_trsm<2>(g, st);
-  if (gmr <= 4) return launch_trsm<4>(g, st);
-  return launch_trsm<8>(g, st);
+  static const int widths[6] = {8, 6, 4, 3, 2, 1};
+  int best = 1;
+  double bu = -1.0;
+  for (int w : widths) {
+    const ix rounds = (gmr + w - 1) / w;
+    const double u = (double)gmr / (double)(w * rounds);
+    if (u > bu + 1e-9) bu = u, best = w;
+  }
+  switch (best) {
+    case 8: return launch_trsm<8>(g, st);
+    case 6: return launch_trsm<6>(g, st);
+    case 4: return launch_trsm<4>(g, st);
+    case 3: return launch_trsm<3>(g, st);
+    case 2: return launch_trsm<2>(g, st);
+    default: return launch_trsm<1>(g, st);
+  }
 }
 
 }  // namespace pb
