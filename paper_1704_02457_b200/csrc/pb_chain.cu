@@ -13,6 +13,8 @@
 // diagonal blocks (pb_tri.cuh) for the factorization and the solve.
 // Restrictions (else the per-stage batched path in chain.py is used):
 // nx, nu multiples of 8, nu == 8 (one 8x8 Lambda block).
+#include <cstdlib>
+
 #include "pb_tri.cuh"
 
 namespace pb {
@@ -274,7 +276,13 @@ cudaError_t run_chain_riccati(const ChainArgs &g, int nx, int nu, cudaStream_t s
     case 8: return launch_chain<1, 2>(g, st);
     case 16: return launch_chain<2, 2>(g, st);
     case 24: return launch_chain<3, 2>(g, st);
-    case 32: return launch_chain<4, 2>(g, st);
+    case 32: {
+      // 4 warps per problem measured best (1.405 -> 1.321 ms at C5), PB_CHAIN_TW for A/B runs
+      static const int tw = getenv("PB_CHAIN_TW") ? atoi(getenv("PB_CHAIN_TW")) : 4;
+      if (tw == 1) return launch_chain<4, 1>(g, st);
+      if (tw == 4) return launch_chain<4, 4>(g, st);
+      return launch_chain<4, 2>(g, st);
+    }
     case 48: return launch_chain<6, 4>(g, st);
     case 64: return launch_chain<8, 4>(g, st);
     default: return cudaErrorInvalidValue;
