@@ -580,16 +580,19 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::N
 // items' A/B(/C) panel runs (16-byte pieces, coalesced across the warp),
 // the product in registers (FMA), coalesced 16-byte stores of D's window.
 
-template <int KMAX>
+template <int KMAX, int STG = 1>
 struct ItemCfg {
   static constexpr int NTH = 128, ITEMS = NTH;
   static constexpr int STRIDE = 3 * 4 * KMAX + 2;  // A, B (4 x KMAX each) + C (4 x 4 <= 4 x KMAX), padded
-  static constexpr size_t SMEM = sizeof(double) * 2 * ITEMS * STRIDE;
+  static constexpr int STAGES = STG;
+  static constexpr size_t SMEM = sizeof(double) * STG * ITEMS * STRIDE;
 };
 
-template <int KMAX, bool SYRK>
+// STG = 1 (single stage, 4 CTAs / 16 warps per SM) measured faster than the
+// 2-stage ring (2 CTAs / 8 warps) at C3 n = 4: more rounds in flight per SM.
+template <int KMAX, bool SYRK, int STG = 1>
 __global__ void __launch_bounds__(128) gemm_item_kernel(GemmArgs g) {
-  using Cfg = ItemCfg<KMAX>;
+  using Cfg = ItemCfg<KMAX, STG>;
   constexpr int ITEMS = Cfg::ITEMS, NTH = Cfg::NTH, STRIDE = Cfg::STRIDE;
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
@@ -625,13 +628,18 @@ __global__ void __launch_bounds__(128) gemm_item_kernel(GemmArgs g) {
     }
   };
 
-  if (blockIdx.x < nrounds) issue(blockIdx.x, 0);
+  if (STG == 2 && blockIdx.x < nrounds) issue(blockIdx.x, 0);
   cp_async_commit();
   int buf = 0;
-  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf ^= 1) {
-    if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x, buf ^= (STG - 1)) {
+    if (STG == 2) {
+      if (rd + gridDim.x < nrounds) issue(rd + gridDim.x, buf ^ 1);
+    } else {
+      issue(rd, 0);
+    }
     cp_async_commit();
-    cp_async_wait<1>();
+    if (STG == 2) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
     double *S = smem + buf * ITEMS * STRIDE + tid * STRIDE;
     double acc[4][4];
@@ -685,10 +693,10 @@ __global__ void __launch_bounds__(128) gemm_item_kernel(GemmArgs g) {
   cp_async_wait<0>();
 }
 
-template <int KMAX, bool SYRK>
+template <int KMAX, bool SYRK, int STG = 1>
 static cudaError_t launch_item(const GemmArgs &g, cudaStream_t st) {
-  using Cfg = ItemCfg<KMAX>;
-  auto kern = gemm_item_kernel<KMAX, SYRK>;
+  using Cfg = ItemCfg<KMAX, STG>;
+  auto kern = gemm_item_kernel<KMAX, SYRK, STG>;
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -802,8 +810,9 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   const bool one_panel = (g.ai & 3) == 0 && (g.bi & 3) == 0 && (g.ci & 3) == 0 && (g.di & 3) == 0 && g.tma && g.tmaC &&
                          ((uintptr_t)g.D.p & 15) == 0 && (g.D.stride & 1) == 0;
   if (big <= 4 && one_panel) {
-    if (g.k <= 4) return launch_item<4, SYRK>(g, st);
-    if (g.k <= 16) return launch_item<16, SYRK>(g, st);
+    // (k <= 4 only: the per-thread staging of larger k does not fit shared memory)
+    static const int item_stg = getenv("PB_ITEM_STG") ? atoi(getenv("PB_ITEM_STG")) : 1;  // A/B switch
+    if (g.k <= 4) return item_stg == 2 ? launch_item<4, SYRK, 2>(g, st) : launch_item<4, SYRK, 1>(g, st);
   }
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
   const ix small = g.m < ncols ? g.m : ncols;

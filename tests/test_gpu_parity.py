@@ -149,7 +149,7 @@ def rand_batch(rng, nb, m, n, fill=None):
     return h
 
 
-GEMM_SHAPES = [(4, 4, 4), (8, 8, 8), (12, 12, 12), (16, 16, 16), (20, 20, 20), (24, 24, 24), (3, 17, 5),
+GEMM_SHAPES = [(4, 4, 4), (4, 4, 8), (3, 2, 16), (4, 3, 13), (8, 8, 8), (12, 12, 12), (16, 16, 16), (20, 20, 20), (24, 24, 24), (3, 17, 5),
                (28, 28, 28), (32, 32, 32), (40, 40, 40), (44, 36, 52), (64, 64, 64), (72, 72, 72), (100, 100, 100),
                (128, 128, 128), (300, 300, 300), (65, 130, 7), (9, 70, 33)]
 
