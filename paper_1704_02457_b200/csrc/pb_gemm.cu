@@ -90,8 +90,8 @@ enum { BOP_NT = 0, BOP_NN = 1, BOP_TRI = 2 };
 // straight from global memory.  Used for tiny items (one tile per item)
 // and as the any-alignment fallback of the NN modes.
 
-template <int MT, int NT, bool SYRK, int BOP = BOP_NT>
-__global__ void __launch_bounds__(256) gemm_direct_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
+template <int MT, int NT, bool SYRK, int BOP = BOP_NT, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
   const int lane = threadIdx.x & 31;
   const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const ix nwarps = (ix)gridDim.x * (blockDim.x >> 5);
@@ -737,7 +737,10 @@ static cudaError_t launch_direct(const GemmArgs &g, cudaStream_t st) {
   const ix cap = (ix)num_sms() * 8 * 8;  // ~8 resident CTAs of 8 warps per SM, a few waves
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  gemm_direct_kernel<MT, NT, SYRK, BOP><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
+  // min 3 CTAs/SM (<= 85 registers): C3 n = 8..24 6.25 -> 4.63 ms summed (n = 16 alone 9 % slower)
+  static const int lb = getenv("PB_DIRECT_LB") ? atoi(getenv("PB_DIRECT_LB")) : 3;  // A/B switch
+  if (lb == 3) gemm_direct_kernel<MT, NT, SYRK, BOP, 3><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
+  else gemm_direct_kernel<MT, NT, SYRK, BOP, 1><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
   note_launch();
   return cudaGetLastError();
 }
