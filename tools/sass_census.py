@@ -26,8 +26,9 @@ def main(lib, out):
     lines = ["# static SASS opcode census of " + lib + " (tools/sass_census.py), per kernel.",
              "# DMMA.8x8x4 = mma.sync m8n8k4 f64 (tcgen05 has no f64 kind), UBLKCP = cp.async.bulk (TMA 1-D),",
              "# UBLKPF = cp.async.bulk.prefetch.L2, SYNCS.* = mbarrier, LDGSTS = cp.async, MUFU.RSQ64H = rsqrt seed."]
-    for k, c in counts.items():
-        name = re.sub(r"^_ZN2pb(?:\d+_GLOBAL__N__\w+?\d+)?", "", k)[:110]
+    names = subprocess.run(["c++filt"], input="\n".join(counts), capture_output=True, text=True).stdout.split("\n")
+    for (k, c), name in zip(counts.items(), names):
+        name = name.replace("(anonymous namespace)::", "")[:120]
         lines.append(name)
         lines.append("    " + ", ".join(f"{op}:{n}" for op, n in sorted(c.items())))
     open(out, "w").write("\n".join(lines) + "\n")
