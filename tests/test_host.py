@@ -84,9 +84,15 @@ def test_level3_bounds_errors_before_launch():
         level3.trsm(2, 2, 1.0, a, a, a, "rltx")
     with pytest.raises(NotImplementedError):
         level3.trsm(2, 2, 1.0, a, a, a, "llnu")
+    with pytest.raises(pb.DimensionError):
+        level3.getrf_pivot(5, 4, a, a)
+    with pytest.raises(pb.DimensionError):
+        level3.getrf_nopivot(4, 4, a.ref(1, 0), a)
     # valid windows on CPU storage: refuses loudly (no CPU fallback)
     with pytest.raises(RuntimeError, match="CUDA"):
         level3.gemm_nt(4, 4, 4, 1.0, a, a, 0.0, a, a)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        level3.getrf_pivot(4, 4, a, a)
 
 
 def _header_symbols():
