@@ -11,7 +11,7 @@
 // Why this shape: the C2 points n = 32 / 64 are HBM-bound (AI 1.3 / 2.6
 // flop/B).  The shared-memory team kernel spent ~3.7K / 9.6K warp
 // instructions per item on staging, index math and barriers
-// (profiles/r01_potrf_reg_ncu.txt).  Here an item costs one pass of loads,
+// (profiles/r01_c2_kernels_ncu.txt).  Here an item costs one pass of loads,
 // register math and one pass of stores:
 //  * tile (i, j), i >= j, of 8x8 elements is one m8n8k4 accumulator: lane
 //    (r = lane/4, q = lane%4) holds (8i + r, 8j + 2q + {0,1}); a warp-wide
