@@ -76,6 +76,16 @@ extern "C" {
 
 int pb_version(void) { return 1; }
 const char *pb_last_error(void) { return t_err.c_str(); }
+// diag_inv of an output holds min(m, n) reciprocals of its matrix; a factor
+// of width w written at column dj needs dj + w of them.  The reference core
+// would write past the end of the diag_inv view (no bounds check,
+// ccore.pyx:1); here it is an argument error.
+static int check_dinv(const pb_dmat_batch *d, int pos, int dj, int w) {
+  const int cap = d->m < d->n ? d->m : d->n;
+  if (dj + w > cap) return fail_arg(pos, "diag_inv too short: dj + n exceeds min(rows, cols) of D");
+  return 0;
+}
+
 int pb_dgetrf(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
               int pivot, int64_t *ipiv, int64_t ipiv_stride, int32_t *info, void *stream) {
   // positions: m1 n2 C3 ci4 cj5 D6 di7 dj8 pivot9 ipiv10 ipiv_stride11 info12 (level3.py:405-446)
@@ -89,6 +99,7 @@ int pb_dgetrf(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dm
   const int mn = m < n ? m : n;
   if (mn == 0 || batch == 0) return 0;  // level3.py:435-436
   if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
+  if ((r = check_dinv(sD, 6, dj, mn))) return r;
   if (pivot && !ipiv) return fail_arg(10, "ipiv is required with pivoting");
   if (pivot && ipiv_stride < mn) return fail_arg(11, "ipiv stride below min(m, n)");
   if (!info) return fail_arg(12, "info is required");
@@ -334,6 +345,7 @@ int pb_dpotrf_l(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_
   if ((r = check_mat(sD, 6, di, dj, m, n, batch, true))) return r;
   if (n == 0 || batch == 0) return 0;  // level3.py:335-336
   if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
+  if ((r = check_dinv(sD, 6, dj, n))) return r;
   if (!info) return fail_arg(9, "info is required");
   return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, (cudaStream_t)stream);
 }
@@ -354,6 +366,7 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
   if ((r = check_mat(sD, 13, di, dj, m, n, batch, true))) return r;
   if (n == 0 || batch == 0) return 0;  // level3.py:370-371
   if (!sD->dA) return fail_arg(13, "output needs diag_inv storage");
+  if ((r = check_dinv(sD, 13, dj, n))) return r;
   if (!info) return fail_arg(16, "info is required");
   cudaStream_t st = (cudaStream_t)stream;
   // k == 0: exactly potrf_l of C (test_level3.py:343-353)

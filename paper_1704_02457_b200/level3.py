@@ -75,6 +75,13 @@ def _mark_diag(mat, dj, n, diagonal):
         mat.diag_lo = mat.diag_hi = 0
 
 
+def _check_dinv(d, dj, w):
+    # the output's diag_inv holds min(rows, cols) reciprocals (matstore.py:88-91);
+    # the reference core would write past its end (unchecked), here it is an error
+    if w > 0 and dj + w > min(d.rows, d.cols):
+        raise DimensionError(f"D.diag_inv too short: dj + n = {dj + w} exceeds min(rows, cols) = {min(d.rows, d.cols)}")
+
+
 def _first_failure(info):
     """(batch_index, index) of the first failing item, or None (host sync)."""
     bad = torch.nonzero(info >= 0)
@@ -229,6 +236,7 @@ def potrf_l(m, C, D, n=None, check=True):
     d, di, dj = _ref(D, "D")
     _check(c, ci, cj, m, n, "C")
     _check(d, di, dj, m, n, "D")
+    _check_dinv(d, dj, n)
     nb = _batch_of(d, c)
     if n == 0 or nb == 0:
         return None
@@ -267,6 +275,7 @@ def syrk_potrf_ln(m, k, A, B, C, D, n=None, check=True):
     _check(b, bi, bj, n, k, "B")
     _check(c, ci, cj, m, n, "C")
     _check(d, di, dj, m, n, "D")
+    _check_dinv(d, dj, n)
     nb = _batch_of(d, a, b, c)
     if n == 0 or nb == 0:
         return None
@@ -296,6 +305,7 @@ def _getrf(m, n, C, D, pivot, ipiv, check, name):
     d, di, dj = _ref(D, "D")
     _check(c, ci, cj, m, n, "C")
     _check(d, di, dj, m, n, "D")
+    _check_dinv(d, dj, min(m, n))
     nb = _batch_of(d, c)
     mn = min(m, n)
     if mn == 0 or nb == 0:

@@ -86,6 +86,9 @@ def test_level3_bounds_errors_before_launch():
         level3.trsm(2, 2, 1.0, a, a, a, "llnu")
     with pytest.raises(pb.DimensionError):
         level3.getrf_pivot(5, 4, a, a)
+    w = pb.allocate_panel_batch(2, 8, 10, device="cpu")
+    with pytest.raises(pb.DimensionError, match="diag_inv"):
+        level3.potrf_l(6, w, w.ref(0, 3))  # diag_inv[3:9] exceeds min(8, 10)
     with pytest.raises(pb.DimensionError):
         level3.getrf_nopivot(4, 4, a.ref(1, 0), a)
     # valid windows on CPU storage: refuses loudly (no CPU fallback)
