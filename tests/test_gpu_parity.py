@@ -930,3 +930,16 @@ def test_riccati_factorize_golden(batch):
             mask[h.diag_off: h.diag_off + ns] = True
             for b in range(batch):
                 compare_storage(got[b], want, mask, ns, f"{r['name']} stage {n} item {b}")
+
+
+def test_randomised_sweep_vs_oracle():
+    """250 random potrf / getrf / gemm / syrk / trsm cases (sizes, window offsets,
+    alpha/beta, failing pivots, batch sizes) against the oracle: FP within
+    50*n*eps on the written window, every other byte and every integer output exact."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "pb_stress", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "stress.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.main(250, 7)

@@ -111,15 +111,64 @@ def gemm_case(rng):
     check(f"gemm {m}x{n}x{k} a={alpha} b={beta}", host(dD), D.storage, mask, max(m, n, k))
 
 
+def syrk_case(rng):
+    m, k = int(rng.integers(1, 90)), int(rng.integers(0, 60))
+    nb = int(rng.integers(1, 20))
+    alpha, beta = float(rng.choice([1.0, -1.0, 0.0])), float(rng.choice([0.0, 1.0, 0.5]))
+    oa, oc, od = ((int(rng.integers(0, 5)), int(rng.integers(0, 3))) for _ in range(3))
+    same = bool(rng.random() < 0.5)
+    A = O.HostBatch(nb, oa[0] + m, oa[1] + max(k, 1))
+    B = A if same else O.HostBatch(nb, oa[0] + m, oa[1] + max(k, 1))
+    C = O.HostBatch(nb, oc[0] + m, oc[1] + m)
+    D = O.HostBatch(nb, od[0] + m + 1, od[1] + m)
+    for X in {id(x): x for x in (A, B, C, D)}.values():
+        X.storage[:] = rng.uniform(-1, 1, X.storage.shape)
+    dA = dev(A)
+    dB = dA if same else dev(B)
+    dC, dD = dev(C), dev(D)
+    level3.syrk_ln(m, k, alpha, dA.ref(*oa), dB.ref(*oa), beta, dC.ref(*oc), dD.ref(*od))
+    O.syrk_ln(m, k, alpha, A, *oa, B, *oa, beta, C, *oc, D, *od)
+    mask = np.zeros(D.storage.shape[1], dtype=bool)
+    for j in range(m):
+        for i in range(j, m):
+            mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+    check(f"syrk {m}x{k} a={alpha} b={beta}", host(dD), D.storage, mask, max(m, k))
+
+
+def trsm_case(rng):
+    m, n = int(rng.integers(1, 90)), int(rng.integers(1, 70))
+    nb = int(rng.integers(1, 20))
+    alpha = float(rng.choice([1.0, -1.0, 0.5]))
+    g = rng.uniform(-1, 1, (nb, n, n))
+    a = np.linalg.cholesky(g @ g.transpose(0, 2, 1) + n * np.eye(n))
+    oa, ob, od = ((int(rng.integers(0, 5)), int(rng.integers(0, 3))) for _ in range(3))
+    A = O.HostBatch(nb, oa[0] + n, oa[1] + n)
+    A.storage[:] = rng.uniform(-1, 1, A.storage.shape)
+    A.set_window(oa[0], oa[1], a)
+    B = O.HostBatch(nb, ob[0] + m, ob[1] + n)
+    D = O.HostBatch(nb, od[0] + m + 1, od[1] + n)
+    for X in (B, D):
+        X.storage[:] = rng.uniform(-1, 1, X.storage.shape)
+    dA, dB, dD = dev(A), dev(B), dev(D)
+    level3.trsm_rltn(m, n, alpha, dA.ref(*oa), dB.ref(*ob), dD.ref(*od))
+    O.trsm_rltn(m, n, alpha, A, *oa, B, *ob, D, *od)
+    mask = np.zeros(D.storage.shape[1], dtype=bool)
+    for j in range(n):
+        for i in range(m):
+            mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+    check(f"trsm {m}x{n}", host(dD), D.storage, mask, max(m, n))
+
+
 def main(cases=300, seed=0):
     rng = np.random.default_rng(seed)
     counts = {}
     for t in range(cases):
-        kind = ("potrf", "getrf", "gemm")[t % 3]
-        {"potrf": potrf_case, "getrf": getrf_case, "gemm": gemm_case}[kind](rng)
+        kinds = ("potrf", "getrf", "gemm", "syrk", "trsm")
+        kind = kinds[t % len(kinds)]
+        {"potrf": potrf_case, "getrf": getrf_case, "gemm": gemm_case, "syrk": syrk_case, "trsm": trsm_case}[kind](rng)
         counts[kind] = counts.get(kind, 0) + 1
     print("stress ok", counts)
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 300)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 300, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
