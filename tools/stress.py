@@ -159,13 +159,62 @@ def trsm_case(rng):
     check(f"trsm {m}x{n}", host(dD), D.storage, mask, max(m, n))
 
 
+def syrk_potrf_case(rng):
+    m, k = int(rng.integers(1, 70)), int(rng.integers(0, 40))
+    nb = int(rng.integers(1, 20))
+    g = rng.uniform(-1, 1, (nb, m, m))
+    c = g @ g.transpose(0, 2, 1) + m * np.eye(m)
+    oa, oc = ((int(rng.integers(0, 5)), int(rng.integers(0, 3))) for _ in range(2))
+    od = (4 * int(rng.integers(0, 2)), int(rng.integers(0, 3)))
+    A = O.HostBatch(nb, oa[0] + m, oa[1] + max(k, 1))
+    A.storage[:] = rng.uniform(-0.3, 0.3, A.storage.shape)
+    C = O.HostBatch(nb, oc[0] + m, oc[1] + m)
+    C.storage[:] = rng.uniform(-1, 1, C.storage.shape)
+    C.set_window(oc[0], oc[1], c)
+    D = O.HostBatch(nb, max(od[0], od[1]) + m + 1, od[1] + m)
+    D.storage[:] = rng.uniform(-1, 1, D.storage.shape)
+    dA, dC, dD = dev(A), dev(C), dev(D)
+    info = level3.syrk_potrf_ln(m, k, dA.ref(*oa), dA.ref(*oa), dC.ref(*oc), dD.ref(*od), check=False)
+    winfo = O.syrk_potrf_ln(m, k, A, *oa, A, *oa, C, *oc, D, *od)
+    if info is not None:
+        assert np.array_equal(info.cpu().numpy(), winfo), ("syrk_potrf info", m, k)
+    mask = np.zeros(D.storage.shape[1], dtype=bool)
+    for j in range(m):
+        for i in range(j, m):
+            mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+    mask[D.diag_off + od[1]: D.diag_off + od[1] + m] = True
+    check(f"syrk_potrf {m}x{k}", host(dD), D.storage, mask, max(m, k))
+
+
+def gemm_nn_case(rng):
+    m, n, k = (int(rng.integers(1, 80)) for _ in range(3))
+    nb = int(rng.integers(1, 16))
+    alpha, beta = float(rng.choice([1.0, -1.0, 0.0])), float(rng.choice([0.0, 1.0]))
+    oa, ob, oc, od = ((int(rng.integers(0, 5)), int(rng.integers(0, 3))) for _ in range(4))
+    A = O.HostBatch(nb, oa[0] + m, oa[1] + k)
+    B = O.HostBatch(nb, ob[0] + k, ob[1] + n)
+    C = O.HostBatch(nb, oc[0] + m, oc[1] + n)
+    D = O.HostBatch(nb, od[0] + m + 1, od[1] + n)
+    for X in (A, B, C, D):
+        X.storage[:] = rng.uniform(-1, 1, X.storage.shape)
+    dA, dB, dC, dD = dev(A), dev(B), dev(C), dev(D)
+    level3.gemm_nn(m, n, k, alpha, dA.ref(*oa), dB.ref(*ob), beta, dC.ref(*oc), dD.ref(*od))
+    O.gemm_nn(m, n, k, alpha, A, *oa, B, *ob, beta, C, *oc, D, *od)
+    mask = np.zeros(D.storage.shape[1], dtype=bool)
+    for j in range(n):
+        for i in range(m):
+            mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
+    check(f"gemm_nn {m}x{n}x{k}", host(dD), D.storage, mask, max(m, n, k))
+
+
 def main(cases=300, seed=0):
     rng = np.random.default_rng(seed)
     counts = {}
     for t in range(cases):
-        kinds = ("potrf", "getrf", "gemm", "syrk", "trsm")
-        kind = kinds[t % len(kinds)]
-        {"potrf": potrf_case, "getrf": getrf_case, "gemm": gemm_case, "syrk": syrk_case, "trsm": trsm_case}[kind](rng)
+        fns = {"potrf": potrf_case, "getrf": getrf_case, "gemm": gemm_case, "syrk": syrk_case, "trsm": trsm_case,
+               "syrk_potrf": syrk_potrf_case, "gemm_nn": gemm_nn_case}
+        kind = list(fns)[t % len(fns)]
+        fns[kind](rng)
         counts[kind] = counts.get(kind, 0) + 1
     print("stress ok", counts)
 
