@@ -7,7 +7,7 @@ leading batch dimension.  Device memory and streams come from PyTorch; all
 arithmetic runs in hand-written sm_100a CUDA kernels behind the C ABI in
 ``include/pb_b200.h`` (``lib/libpb_b200.so``).  There is no CPU fallback.
 """
-from . import level3, pack
+from . import fixtures, level3, pack
 from ._native import lib_path, load as load_native
 from .errors import (DimensionError, FactorizationError, MemoryLayoutError,
                      NotPositiveDefiniteError, PanelBlasError, SingularMatrixError)
@@ -26,7 +26,7 @@ def backend_name():
 
 __all__ = [
     "ALIGN", "PS", "ColBatch", "PanelBatch", "SubRef", "allocate_panel_batch", "backend_name",
-    "create_panel_batch", "element_offset", "level3", "lib_path", "load_native",
+    "create_panel_batch", "element_offset", "fixtures", "level3", "lib_path", "load_native",
     "memsize_panel_batch", "memsize_panel_matrix", "pack",
     "DimensionError", "FactorizationError", "MemoryLayoutError", "NotPositiveDefiniteError",
     "PanelBlasError", "SingularMatrixError",

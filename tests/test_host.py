@@ -8,6 +8,7 @@ include/pb_b200.h declares.
 import ctypes
 import os
 import re
+import struct
 
 import numpy as np
 import pytest
@@ -158,3 +159,34 @@ def test_bench_csv_matches_reference_schema(tmp_path):
     ms = [int(r[2]) for r in rows]
     assert ms == sorted(ms) and rows[0][0] == "potrf_l" and rows[0][1] == "b200"
     assert float(rows[0][5]) == (1.0 / 1e3) / 1000 and float(rows[-1][6]) == 70.0
+
+
+def test_fixture_formats_match_the_reference(tmp_path):
+    """§8f row 3: the matrix / OCP text fixtures written by the REFERENCE's own
+    writers (tests/golden/make_fixture_golden.py) read back bit-exactly and
+    are reproduced byte for byte by this package's writers."""
+    from paper_1704_02457_b200 import fixtures
+    gold = os.path.join(REPO, "tests", "golden")
+    ref = open(os.path.join(gold, "ref_matrix_fixture.txt")).read()
+    mat = fixtures.read_fixture(os.path.join(gold, "ref_matrix_fixture.txt"), device="cpu")
+    assert (mat.rows, mat.cols) == (5, 3)
+    lines = ref.splitlines()[1:]
+    for i, line in enumerate(lines):
+        for j, tok in enumerate(line.split()):
+            got = mat.storage[0, pb.element_offset(i, j, 4, mat.panel_length)].item()
+            assert struct.pack("<d", got) == struct.pack("<d", float(tok))
+    out = tmp_path / "m.txt"
+    fixtures.write_fixture(out, mat)
+    assert out.read_text() == ref
+    # a window of a larger batch item, and failing-item dumps
+    big = pb.allocate_panel_batch(3, 9, 7, device="cpu", zero=True)
+    for b in range(3):
+        big.storage[b, :] = float(b)
+    paths = fixtures.dump_failures(tmp_path / "fail", big, [-1, 4, -1], ai=2, aj=3, m=5, n=3)
+    assert len(paths) == 1 and paths[0].endswith("item_1.txt")
+    assert open(paths[0]).read() == ref.splitlines()[0] + "\n" + "\n".join(["1 1 1"] * 5) + "\n"
+    nx, nu, stages, P = fixtures.read_ocp_fixture(os.path.join(gold, "ref_ocp_fixture.txt"))
+    assert (nx, nu, len(stages), P.shape) == (2, 1, 2, (2, 2))
+    out2 = tmp_path / "ocp.txt"
+    fixtures.write_ocp_fixture(out2, nx, nu, stages, P)
+    assert out2.read_text() == open(os.path.join(gold, "ref_ocp_fixture.txt")).read()
