@@ -509,6 +509,8 @@ def run_ours(args):
         print(json.dumps(line))
         if args.csv:
             emit_csv(csv_rows(points, pts), args.csv)
+        if args.csv_ext:
+            emit_csv_ext(csv_rows(points, pts), points, pts, world, args.csv_ext)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -537,6 +539,19 @@ def emit_csv(rows, path):
         fh.write("routine,impl,m,n,k,seconds,gflops\n")
         for r in sorted(rows, key=lambda r: (r[0], r[1], r[2])):
             fh.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.17g},{r[6]:.17g}\n")
+
+
+def emit_csv_ext(rows, points, pts, world, path):
+    """The reference's seven columns (same order and formatting) followed by
+    gpus, batch, hbm_gbs_alg, roofline_gflops, roofline_frac (SURVEY §8f row 3);
+    a separate file, because the reference's parse_csv accepts only its exact header."""
+    with open(path, "w") as fh:
+        fh.write("routine,impl,m,n,k,seconds,gflops,gpus,batch,hbm_gbs_alg,roofline_gflops,roofline_frac\n")
+        order = sorted(range(len(rows)), key=lambda i: (rows[i][0], rows[i][1], rows[i][2]))
+        for i in order:
+            r, p, pt = rows[i], points[i], pts[i]
+            fh.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.17g},{r[6]:.17g},{world},{pt.batch * world},"
+                     f"{p['hbm_gbs_alg']:.17g},{p['roofline_gflops']:.17g},{p['roofline_frac']:.17g}\n")
 
 
 def traffic_from_profile(pt):
@@ -880,6 +895,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=14.0)
     ap.add_argument("--ref-seconds", type=float, default=7.0)
     ap.add_argument("--csv", default=None, help="also write per-point rows in the reference's sweep CSV schema")
+    ap.add_argument("--csv-ext", default=None,
+                    help="also write the reference's columns + gpus, batch, algorithmic GB/s and roofline fraction")
     ap.add_argument("--only", default=None,
                     help="comma-separated point labels to keep (tuning runs only, e.g. 'potrf_l n=4')")
     args = ap.parse_args()

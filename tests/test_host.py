@@ -159,6 +159,15 @@ def test_bench_csv_matches_reference_schema(tmp_path):
     ms = [int(r[2]) for r in rows]
     assert ms == sorted(ms) and rows[0][0] == "potrf_l" and rows[0][1] == "b200"
     assert float(rows[0][5]) == (1.0 / 1e3) / 1000 and float(rows[-1][6]) == 70.0
+    # extended sidecar: the same seven columns, then gpus, batch, GB/s, roofline
+    for i, p in enumerate(points):
+        p.update(hbm_gbs_alg=100.0 * (i + 1), roofline_gflops=1000.0, roofline_frac=0.01 * (i + 1))
+    ext = tmp_path / "sweep_ext.csv"
+    bench.emit_csv_ext(bench.csv_rows(points, pts), points, pts, 2, str(ext))
+    el = ext.read_text().splitlines()
+    assert el[0].startswith(lines[0] + ",gpus,batch,")
+    assert [e.split(",")[:7] for e in el[1:]] == rows
+    assert el[1].split(",")[7] == "2" and int(el[1].split(",")[8]) == 2 * pts[0].batch
 
 
 def test_fixture_formats_match_the_reference(tmp_path):
