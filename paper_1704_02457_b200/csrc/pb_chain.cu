@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
   using Cfg = ChainCfg<NXB, TW>;
   constexpr int NB = Cfg::NB, NS = Cfg::NS, NX = Cfg::NX;
   extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform();
   const int team = warp / TW, tw = warp % TW;
   const int teams_per_cta = (blockDim.x >> 5) / TW;
   const int tthreads = TW * 32, ttid = tw * 32 + lane;

@@ -17,6 +17,12 @@ namespace pb {
 
 typedef int64_t ix;
 
+// Warp index as a value the compiler can prove warp-uniform (a shuffle from
+// lane 0).  Derived straight from threadIdx it is not, so every shuffle / MMA
+// inside a warp-dependent branch got WARPSYNC + collective fix-up code (the
+// n = 128 potrf team kernel: 1622 -> 854 IMAD, 123 WARPSYNC -> 0).
+__device__ __forceinline__ int warp_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
 __host__ __device__ __forceinline__ ix eo(ix i, ix j, ix cn) { return (i & ~(ix)3) * cn + 4 * j + (i & 3); }
 
 // Per-launch view of one operand: item base pointer + stride + panel length.

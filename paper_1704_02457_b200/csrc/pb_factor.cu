@@ -203,7 +203,7 @@ __device__ __forceinline__ void add_block_tiles(double (&a)[MAXT][2], const doub
 template <int TW, int MAXT, bool DB, int GM = 0, int GN = 0, bool SK = false, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) potrf_team_kernel(PotrfArgs g, int team_elems, int vec_in, int vec_out) {
   extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform();
   const int team = warp / TW, tw = warp % TW;
   const int teams_per_cta = (blockDim.x >> 5) / TW;
   const int tthreads = TW * 32, ttid = tw * 32 + lane;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(256, MINB) potrf_team_kernel(PotrfArgs g, int 
 template <int TW>
 __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_elems, int vec_in) {
   extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform();
   const int team = warp / TW, tw = warp % TW;
   const int teams_per_cta = (blockDim.x >> 5) / TW;
   const int tthreads = TW * 32, ttid = tw * 32 + lane;

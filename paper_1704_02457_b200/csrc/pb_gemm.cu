@@ -93,7 +93,7 @@ enum { BOP_NT = 0, BOP_NN = 1, BOP_TRI = 2 };
 template <int MT, int NT, bool SYRK, int BOP = BOP_NT, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
   const int lane = threadIdx.x & 31;
-  const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + warp_uniform();
   const ix nwarps = (ix)gridDim.x * (blockDim.x >> 5);
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / k-col
   const ix ncols = SYRK ? g.m : g.n;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(TiledCfg<BM, BN, WM, WN, KC, STAGES>::NTHREADS
   using Cfg = TiledCfg<BM, BN, WM, WN, KC, STAGES>;
   constexpr int MT = Cfg::MT, NT = Cfg::NT;
   extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform();
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int fr = lane >> 2, fc = lane & 3;
 
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::N
   uint64_t *empty = full + STAGES;
   uint64_t *cfull = empty + STAGES;
   uint64_t *cempty = cfull + CB;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform();
   const ix ncols = SYRK ? g.m : g.n;
   const bool cin = CB > 0 && BOP != BOP_TRI && g.beta != 0.0 && g.tmaC;  // C through shared memory
   const bool domma = g.alpha != 0.0 || BOP == BOP_TRI;
