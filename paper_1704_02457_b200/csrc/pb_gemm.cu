@@ -393,19 +393,6 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::N
       const ix u = blockIdx.x + ul * gridDim.x;
       ix b, tm, tn;
       unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
-      if (CB > 0 && cin) {
-        const int cb = (int)(ul % (CB > 0 ? CB : 1));
-        if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / (CB > 0 ? CB : 1)) - 1) & 1));
-        const ix rc = g.ci + tm * BM;
-        const ix rows = min((ix)BM, g.m - tm * BM), cols = min((ix)BN, ncols - tn * BN);
-        const int npc = (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1);
-        const unsigned bytes = 32u * (unsigned)cols;
-        if (lane == 0) mbar_arrive_expect_tx(&cfull[cb], bytes * npc);
-        __syncwarp();
-        const double *C = g.C.item(b) + (rc >> 2) * 4 * g.C.cn + 4 * (g.cj + tn * BN);
-        for (int p = lane; p < npc; p += 32)
-          tma_load_1d(cbuf + cb * Cfg::C_ELEMS + p * 4 * BN, C + (ix)p * 4 * g.C.cn, bytes, &cfull[cb]);
-      }
       for (ix ch = first_chunk<BN, KC, BOP>(tn); ch < nk; ++ch, ++s) {
         const int st = (int)(s % STAGES);
         if (s >= STAGES) mbar_wait(&empty[st], (unsigned)(((s / STAGES) - 1) & 1));
@@ -442,6 +429,22 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::N
             else tma_load_1d(sb + (p - npa) * 4 * BN, B + (ix)(p - npa) * 4 * g.B.cn, bytesb, &full[st]);
           }
         }
+      }
+      // the unit's C tile after its A/B chunks: with one C buffer its
+      // issue waits for the previous unit's epilogue, which must not hold
+      // back this unit's operand loads
+      if (CB > 0 && cin) {
+        const int cb = (int)(ul % (CB > 0 ? CB : 1));
+        if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / (CB > 0 ? CB : 1)) - 1) & 1));
+        const ix rc = g.ci + tm * BM;
+        const ix rows = min((ix)BM, g.m - tm * BM), cols = min((ix)BN, ncols - tn * BN);
+        const int npc = (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1);
+        const unsigned bytes = 32u * (unsigned)cols;
+        if (lane == 0) mbar_arrive_expect_tx(&cfull[cb], bytes * npc);
+        __syncwarp();
+        const double *C = g.C.item(b) + (rc >> 2) * 4 * g.C.cn + 4 * (g.cj + tn * BN);
+        for (int p = lane; p < npc; p += 32)
+          tma_load_1d(cbuf + cb * Cfg::C_ELEMS + p * 4 * BN, C + (ix)p * 4 * g.C.cn, bytes, &cfull[cb]);
       }
     }
     return;
@@ -839,7 +842,14 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
     if (force_t) T = force_t;
     const bool k40 = g.k > 32 && g.k <= 40;
     const bool cs = g.beta != 0.0 && g.tmaC;  // C tile through shared memory
-#define PB_TMA(T_, WM_, WN_, K_)                                                     \
+    static const char *tcfg = getenv("PB_TMA_CS");  // A/B switch for the beta != 0 pipeline shape
+    if (tcfg && cs && T == 64 && !k40) {
+      const std::string v(tcfg);
+      if (v == "k16s4") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 1>(g, st);
+      if (v == "k16s3") return launch_tma<64, 64, 32, 16, 16, 3, SYRK, 1>(g, st);
+      if (v == "k8s6") return launch_tma<64, 64, 32, 16, 8, 6, SYRK, 1>(g, st);
+    }
+#define PB_TMA(T_, WM_, WN_, K_)                                                    \
   if (T == T_ && (K_ == 40) == k40) {                                                \
     if (cs) return launch_tma<T_, T_, WM_, WN_, K_, 2, SYRK, 1>(g, st);              \
     return launch_tma<T_, T_, WM_, WN_, K_, 3, SYRK, 0>(g, st);                      \
