@@ -943,3 +943,42 @@ def test_randomised_sweep_vs_oracle():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     mod.main(250, 7)
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64])
+def test_potrf_host_pinned_descriptors(n):
+    """The C ABI also takes pinned (UVA-mapped) HOST storage: the kernels read
+    C and write D across PCIe.  Same bytes as the oracle (bit-exact for
+    n <= 16, tolerance above), info identical, and every byte outside the
+    reference's write set -- D's strict upper, padding -- unchanged in host
+    memory (profiles/r01_pcie_zero_copy.txt)."""
+    import ctypes
+    from paper_1704_02457_b200 import _native
+    rng = np.random.default_rng(300 + n)
+    nb = 41
+    a = spd_batch(rng, nb, n)
+    a[5, n // 2, n // 2] = -1.0
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    D = rand_batch(rng, nb, n, n, fill=-3.25)
+    hC = torch.from_numpy(C.storage.copy()).pin_memory()
+    hD = torch.from_numpy(D.storage.copy()).pin_memory()
+    pC, pD = pb.create_panel_batch(nb, n, n, hC), pb.create_panel_batch(nb, n, n, hD)
+    dc, dd = pC.descriptor(), pD.descriptor()
+    info = torch.empty(nb, dtype=torch.int32, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert _native.call("pb_dpotrf_l", n, n, ctypes.byref(dc), 0, 0, ctypes.byref(dd), 0, 0,
+                        ctypes.c_void_p(info.data_ptr()), st) == 0
+    torch.cuda.synchronize()
+    winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
+    assert np.array_equal(info.cpu().numpy(), winfo)
+    got = hD.numpy()
+    if n <= 16:
+        assert np.array_equal(got.view(np.uint64), D.storage.view(np.uint64))
+    else:
+        mask = np.zeros(D.storage.shape[1], dtype=bool)
+        for i in range(n):
+            for j in range(i + 1):
+                mask[pb.element_offset(i, j, 4, pD.panel_length)] = True
+        mask[pD._diag_off:pD._diag_off + n] = True
+        compare_storage(got, D.storage, mask, n, f"host-pinned n={n}")
