@@ -982,3 +982,33 @@ def test_potrf_host_pinned_descriptors(n):
                 mask[pb.element_offset(i, j, 4, pD.panel_length)] = True
         mask[pD._diag_off:pD._diag_off + n] = True
         compare_storage(got, D.storage, mask, n, f"host-pinned n={n}")
+
+
+@pytest.mark.parametrize("op,m,n,k,nb", [("gemm", 64, 64, 100, 3000), ("gemm", 48, 48, 70, 2000),
+                                         ("syrk", 96, 96, 40, 1500), ("syrk", 64, 64, 130, 1200)])
+def test_tma_pipeline_many_units_per_cta_beta1(op, m, n, k, nb):
+    """beta != 0 through the warp-specialised TMA pipeline with many units per
+    CTA and several k-chunks per unit (the producer streams A/B chunks and the
+    C tile of consecutive units through shared rings): every item of a large
+    batch against a dense fp64 torch reference, written window only."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = pb.allocate_panel_batch(nb, m, k)
+    B = A if op == "syrk" else pb.allocate_panel_batch(nb, n, k)
+    C = pb.allocate_panel_batch(nb, m, n)
+    for x in {id(x): x for x in (A, B, C)}.values():
+        x.storage.uniform_(-1, 1, generator=g)
+    D = pb.allocate_panel_batch(nb, m, n)
+    D.storage.fill_(-7.5)
+    if op == "gemm":
+        level3.gemm_nt(m, n, k, -0.5, A, B, 1.0, C, D)
+    else:
+        level3.syrk_ln(m, k, -0.5, A, A, 1.0, C, D)
+    a, b, c = pack.unpack_window(A, m, k), pack.unpack_window(B, n, k), pack.unpack_window(C, m, n)
+    want = -0.5 * torch.bmm(a, b.transpose(1, 2)) + c
+    got = pack.unpack_window(D, m, n)
+    if op == "syrk":
+        low = torch.tril(torch.ones(m, n, dtype=torch.bool, device="cuda"))
+        assert bool((got[:, ~low] == -7.5).all())  # strict upper untouched
+        got, want = got[:, low], want[:, low]
+    err = (torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)).item()
+    assert err <= 50 * max(m, n, k) * EPS, err
