@@ -123,28 +123,40 @@ __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix t
     if (g.alpha != 0.0 || BOP == BOP_TRI) {
       // triangular B: rows above this tile's first column are all zero
       const ix kstart = BOP == BOP_TRI ? (cbase & ~(ix)3) : 0;
-      for (ix k0 = kstart; k0 < g.k; k0 += 4) {
-        const ix l = k0 + fc;
-        double a[MT], bb[NT];
+      // KU k-steps of fragments are loaded before their DMMAs, so a unit
+      // exposes one global-load latency per 4*KU columns, not one per 4
+      constexpr int KU = MT * NT <= 2 ? 4 : (MT * NT <= 4 ? 2 : 1);
+      for (ix k0 = kstart; k0 < g.k; k0 += 4 * KU) {
+        double a[KU][MT], bb[KU][NT];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const ix r = rbase + 8 * i + fr;
-          a[i] = (r < g.m && l < g.k) ? ldg_nc(A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
+        for (int u = 0; u < KU; ++u) {
+          const ix l = k0 + 4 * u + fc;
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const ix r = rbase + 8 * i + fr;
+            a[u][i] = (r < g.m && l < g.k) ? ldg_nc(A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const ix r = cbase + 8 * j + fr;
+            if (BOP == BOP_NT)
+              bb[u][j] = (r < ncols && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
+            else
+              bb[u][j] = (r < ncols && l < g.k && (BOP != BOP_TRI || l >= r))
+                             ? ldg_nc(B + eo(g.bi + l, g.bj + r, g.B.cn))
+                             : 0.0;
+          }
         }
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const ix r = cbase + 8 * j + fr;
-          if (BOP == BOP_NT)
-            bb[j] = (r < ncols && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
-          else
-            bb[j] = (r < ncols && l < g.k && (BOP != BOP_TRI || l >= r)) ? ldg_nc(B + eo(g.bi + l, g.bj + r, g.B.cn))
-                                                                         : 0.0;
+        for (int u = 0; u < KU; ++u) {
+          if (k0 + 4 * u < g.k) {  // no zero-fragment steps past k (keeps -0.0 results exact)
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j)
+                if (!SYRK || j <= i) dmma(acc[i][j], a[u][i], bb[u][j]);
+          }
         }
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int j = 0; j < NT; ++j)
-            if (!SYRK || j <= i) dmma(acc[i][j], a[i], bb[j]);
       }
     }
 #pragma unroll
