@@ -57,6 +57,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ double ldg_nc(const double *p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldg_nc2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) ----
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }

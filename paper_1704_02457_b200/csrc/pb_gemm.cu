@@ -729,6 +729,94 @@ static cudaError_t launch_item(const GemmArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// gemm_item_reg: the same one-thread-per-item product with no shared-memory
+// staging: every thread loads its item's A/B(/C) panel runs straight into
+// registers with 16-byte loads (all of an item's bytes are used by the one
+// thread, so every fetched sector is consumed), computes, and stores its own
+// window.  With no round barrier every warp keeps ~8 KB of loads in flight,
+// which the staged kernel's load / compute / store rounds could not.
+template <bool SYRK, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) gemm_item_reg_kernel(GemmArgs g) {
+  const int m = (int)g.m, n = (int)g.n, k = (int)g.k;
+  const bool rc = g.beta != 0.0, ab = g.alpha != 0.0;
+  for (ix b = (ix)blockIdx.x * blockDim.x + threadIdx.x; b < g.batch; b += (ix)gridDim.x * blockDim.x) {
+    double av[4][4], bv[4][4], cv[4][4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const bool ok = ab && l < k;
+      double2 a01 = make_double2(0.0, 0.0), a23 = a01, b01 = a01, b23 = a01;
+      if (ok) {
+        const double *A = g.A.item(b) + eo(g.ai, g.aj + l, g.A.cn);
+        const double *B = g.B.item(b) + eo(g.bi, g.bj + l, g.B.cn);
+        a01 = ldg_nc2(A), a23 = ldg_nc2(A + 2);
+        b01 = ldg_nc2(B), b23 = ldg_nc2(B + 2);
+      }
+      av[l][0] = a01.x, av[l][1] = a01.y, av[l][2] = a23.x, av[l][3] = a23.y;
+      bv[l][0] = b01.x, bv[l][1] = b01.y, bv[l][2] = b23.x, bv[l][3] = b23.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2 c01 = make_double2(0.0, 0.0), c23 = c01;
+      if (rc && j < n) {
+        const double *C = g.C.item(b) + eo(g.ci, g.cj + j, g.C.cn);
+        c01 = ldg_nc2(C), c23 = ldg_nc2(C + 2);
+      }
+      cv[0][j] = c01.x, cv[1][j] = c01.y, cv[2][j] = c23.x, cv[3][j] = c23.y;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      if (ab && l < k) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[l][i], bv[l][j], acc[i][j]);
+      }
+    if (g.skip && g.skip[b] >= 0) continue;
+    double *D = g.D.item(b);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < n) {
+      double v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v[i] = (SYRK && (i >> 2) == (j >> 2)) ? syrk_diag_rule(g.alpha, acc[i][j], g.beta, cv[i][j])
+                                               : store_rule(g.alpha, acc[i][j], g.beta, cv[i][j]);
+      double *dst = D + eo(g.di, g.dj + j, g.D.cn);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r0 = 2 * h;
+        const bool w0 = r0 < m && (!SYRK || r0 >= j), w1 = r0 + 1 < m && (!SYRK || r0 + 1 >= j);
+        if (w0 && w1) *reinterpret_cast<double2 *>(dst + r0) = make_double2(v[r0], v[r0 + 1]);
+        else if (w0) dst[r0] = v[r0];
+        else if (w1) dst[r0 + 1] = v[r0 + 1];
+      }
+      }
+    }
+  }
+}
+
+template <bool SYRK, int MINB = 1>
+static cudaError_t launch_item_reg(const GemmArgs &g, cudaStream_t st) {
+  auto kern = gemm_item_reg_kernel<SYRK, MINB>;
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+    if (occ < 1) occ = 1;
+  }
+  ix grid = (ix)num_sms() * occ;
+  const ix need = (g.batch + 127) / 128;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 128, 0, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // host dispatch
 
@@ -832,6 +920,9 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
   if (big <= 4 && one_panel) {
     // (k <= 4 only: the per-thread staging of larger k does not fit shared memory)
     static const int item_stg = getenv("PB_ITEM_STG") ? atoi(getenv("PB_ITEM_STG")) : 1;  // A/B switch
+    // register-direct kernel (C3 n = 4: 3.40 -> 3.01 ms; capping it at 4-6 CTAs/SM spills and is slower)
+    static const int item_reg = getenv("PB_ITEM_REG") ? atoi(getenv("PB_ITEM_REG")) : 1;  // A/B switch
+    if (g.k <= 4 && item_reg) return launch_item_reg<SYRK>(g, st);
     if (g.k <= 4) return item_stg == 2 ? launch_item<4, SYRK, 2>(g, st) : launch_item<4, SYRK, 1>(g, st);
   }
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
