@@ -125,9 +125,10 @@ __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix t
       const ix kstart = BOP == BOP_TRI ? (cbase & ~(ix)3) : 0;
       // KU k-steps of fragments are loaded before their DMMAs, so a unit
       // exposes one global-load latency per 4*KU columns, not one per 4
-      // (measured on the C3 sweep: KU = 2 for the 3x3-tile units is faster
-      // even with the few spills it costs at the 85-register cap)
-      constexpr int KU = MT * NT <= 2 ? 4 : 2;
+      // (measured on the C3 sweep: KU = 4 up to 2x2 tiles, KU = 2 for the
+      // 3x3-tile units, faster even with the few spills it costs at the
+      // 85-register cap)
+      constexpr int KU = MT * NT <= 4 ? 4 : 2;
       for (ix k0 = kstart; k0 < g.k; k0 += 4 * KU) {
         double a[KU][MT], bb[KU][NT];
 #pragma unroll
