@@ -900,6 +900,7 @@ def main():
     ap.add_argument("--only", default=None,
                     help="comma-separated point labels to keep (tuning runs only, e.g. 'potrf_l n=4')")
     args = ap.parse_args()
+    config_points(args.config)  # reject an unknown --config before touching CUDA
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

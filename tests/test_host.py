@@ -199,3 +199,64 @@ def test_fixture_formats_match_the_reference(tmp_path):
     out2 = tmp_path / "ocp.txt"
     fixtures.write_ocp_fixture(out2, nx, nu, stages, P)
     assert out2.read_text() == open(os.path.join(gold, "ref_ocp_fixture.txt")).read()
+
+
+def test_bench_flop_counts_follow_the_reference():
+    """bench.Point.flops_item restates the reference's flop_count
+    (pkg/src/panelblas/bench.py:85-105); KATs after its
+    tests/test_bench.py:13-21, plus bench.memsize == the matstore size."""
+    import sys
+    sys.path.insert(0, REPO)
+    import bench
+    f = lambda op, m, n, k: bench.Point(op, m, n, k, 1).flops_item  # noqa: E731
+    assert f("gemm_nt", 100, 100, 100) == 2e6
+    assert f("gemm_nn", 0, 5, 5) == 0.0
+    assert f("potrf_l", 3, 3, 3) == 9.0
+    assert f("syrk_ln", 4, 4, 3) == 4 * 5 * 3
+    assert f("trsm_rltn", 6, 4, 0) == 6 * 16
+    assert f("trmm_rlnn", 6, 4, 0) == 6 * 16
+    assert f("syrk_potrf_ln", 4, 4, 3) == 4 * 5 * 3 + 64 / 3.0
+    assert f("getrf", 3, 3, 0) == 18.0
+    nx, nu, N, s = 32, 8, 50, 40
+    assert f("riccati_fact", nx, nu, N) == N * (s * nx * nx + s * (s + 1) * nx + s ** 3 / 3.0)
+    with pytest.raises(ValueError):
+        bench.Point("nope", 1, 1, 1, 1)
+    for m in range(0, 41):
+        for n in range(0, 41, 3):
+            assert bench.memsize(m, n) == memsize_panel_matrix(m, n)
+    # every C2 point carries ~2^34 flops (BASELINE configs[1])
+    pts, _ = bench.config_points("c2")
+    assert [p.n for p in pts] == [4, 8, 16, 32, 64, 128, 256]
+    for p in pts:
+        assert abs(p.batch * p.flops_item / 2 ** 34 - 1) < 1e-3
+
+
+def _run_bench(*args, env=None):
+    import subprocess
+    import sys
+    e = dict(os.environ, **(env or {}))
+    return subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), *args], capture_output=True,
+                          text=True, timeout=240, env=e)
+
+
+def test_bench_cli_reference_arm_and_exit_codes():
+    """bench.py CLI in a subprocess, after the reference's test_bench.py:147-171:
+    the reference arm (host cores only, bounded sample) prints ONE JSON line
+    with the contract keys; non-zero ranks exit 0 silently; an unknown
+    --config exits non-zero before any CUDA call."""
+    import json
+    r = _run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-seconds", "0.05",
+                   "--only", "potrf_l n=4,potrf_l n=8")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "GFLOP/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("reference", "port")
+    r1 = _run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", env={"RANK": "1", "WORLD_SIZE": "2"})
+    assert r1.returncode == 0 and r1.stdout.strip() == ""
+    rb = _run_bench("--config", "bogus")
+    assert rb.returncode != 0 and "unknown config" in rb.stderr
