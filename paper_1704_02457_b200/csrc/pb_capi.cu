@@ -68,6 +68,21 @@ static bool tma_ok(const pb_dmat_batch *x) { return ((uintptr_t)x->pA & 15) == 0
 
 static int finish(cudaError_t e) { return e == cudaSuccess ? 0 : cuda_fail(e); }
 
+// The device's default stream-ordered pool would otherwise return its pages
+// at every synchronize (release threshold 0) and re-map them on the next
+// call's cudaMallocAsync -- milliseconds per GB of scratch.
+static void keep_pool_reserved() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 }  // namespace pb
 
 using namespace pb;
@@ -195,6 +210,7 @@ int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
     memset(&w, 0, sizeof w);
     w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
     w.stride = (int64_t)((m + 3) & ~3) * w.cn;
+    keep_pool_reserved();
     if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
     w.pA = wp;
     CopyArgs c;
@@ -300,9 +316,43 @@ int pb_dtrsm_rltn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
 
 // ---- potrf_l ------------------------------------------------------------
 
+// Blocked-driver failure fix-up.  The reference factors row panel by row
+// panel (ccore.pyx:877-905): an item failing in row panel p leaves D's rows
+// past p untouched.  The blocked driver writes the whole tall panel first,
+// so it snapshots D's rows [n1, m) x cols [0, n1) and, for items that then
+// fail in the trailing block, puts back the rows below the failing row panel.
+// save = true: S <- D for every item; save = false: D <- S where needed.
+__global__ void potrf_blk_snapshot(Mat D, ix di, ix dj, ix m, ix n1, double *S, const int32_t *info, int off,
+                                   bool save) {
+  const ix b = blockIdx.x;
+  ix r0 = n1;
+  if (!save) {
+    const int f = info[b] - off;
+    if (info[b] < 0 || f < n1) return;  // healthy, or failed before / inside the panel (panel kernel's writes)
+    r0 = (ix)(f / 4) * 4 + 4;           // reference writes row panel f/4 (off-diagonal blocks), nothing below
+  }
+  double *d = D.p + b * D.stride;
+  double *sv = S + b * (m - n1) * n1;
+  // storage order (row quad, column, row in quad): consecutive threads touch
+  // consecutive doubles of a panel when di is panel-aligned
+  const ix q0 = r0 / 4, nq = (m + 3) / 4;
+  for (ix e = threadIdx.x; e < (nq - q0) * n1 * 4; e += blockDim.x) {
+    const ix r = (q0 + e / (4 * n1)) * 4 + (e & 3), c = (e >> 2) % n1;
+    if (r >= m) continue;
+    double *pd = d + eo(di + r, dj + c, D.cn);
+    double *ps = sv + (r - n1) * n1 + c;
+    if (save) *ps = *pd;
+    else *pd = *ps;
+  }
+}
+
 static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
                      int32_t *info, int merge, int off, cudaStream_t st) {
-  if (potrf_fits(m, n)) {
+  // PB_POTRF_BLOCK=b splits any n >= 2b into a b-column panel + syrk + trailing factor (0 = only when the
+  // item does not fit one team); default 128 (n=256: 2.27 -> 2.18 ms, profiles/r01_potrf_blocked_failfix.txt)
+  static const int blk = getenv("PB_POTRF_BLOCK") ? atoi(getenv("PB_POTRF_BLOCK")) : 128;
+  const bool split = blk >= 8 && blk % 8 == 0 && n >= 2 * blk && potrf_fits(m, blk);
+  if (!split && potrf_fits(m, n)) {
     PotrfArgs g;
     g.m = m, g.n = n;
     g.C = to_mat(sC), g.D = to_mat(sD);
@@ -317,20 +367,44 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
   // the trailing block, recursive factor of the trailing block.
   int n1 = 8;
   while (n1 + 8 < n && potrf_fits(m, n1 + 8)) n1 += 8;
+  if (split) n1 = blk;
   int r;
-  if ((r = potrf_run(m, n1, sC, ci, cj, sD, di, dj, info, merge, off, st))) return r;
+  const int batch = sD->batch;
+  // trailing-block downdate goes to scratch T (not D) so a failing item's D
+  // keeps its bytes past the failure; snapshot of D's panel rows below n1
+  const int tm = m - n1, tn = n - n1;
+  pb_dmat_batch T{};
+  T.m = tm, T.n = tn, T.cn = (tn + 3) / 4 * 4, T.batch = batch;
+  T.stride = (int64_t)((tm + 3) / 4 * 4) * T.cn;
+  double *snap = nullptr;
+  keep_pool_reserved();
+  if ((r = finish(cudaMallocAsync((void **)&T.pA, sizeof(double) * (size_t)T.stride * batch, st)))) return r;
+  if ((r = finish(cudaMallocAsync((void **)&snap, sizeof(double) * (size_t)tm * n1 * batch, st)))) {
+    cudaFreeAsync(T.pA, st);
+    return r;
+  }
+  auto release = [&](int rc) {
+    cudaFreeAsync(T.pA, st);
+    cudaFreeAsync(snap, st);
+    return rc;
+  };
+  const Mat dm = to_mat(sD);
+  potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, true);
+  if ((r = potrf_run(m, n1, sC, ci, cj, sD, di, dj, info, merge, off, st))) return release(r);
   GemmArgs g;
-  g.m = m - n1, g.n = m - n1, g.k = n1, g.alpha = -1.0, g.beta = 1.0;
-  g.A = to_mat(sD), g.B = to_mat(sD), g.C = to_mat(sC), g.D = to_mat(sD);
-  g.ai = di + n1, g.aj = dj, g.bi = di + n1, g.bj = dj, g.ci = ci + n1, g.cj = cj + n1, g.di = di + n1,
-  g.dj = dj + n1;
+  // trailing trapezoid: m - n1 rows, n - n1 columns (syrk tiles cover m - n1 columns, stores clip to g.n)
+  g.m = m - n1, g.n = n - n1, g.k = n1, g.alpha = -1.0, g.beta = 1.0;
+  g.A = to_mat(sD), g.B = to_mat(sD), g.C = to_mat(sC), g.D = to_mat(&T);
+  g.ai = di + n1, g.aj = dj, g.bi = di + n1, g.bj = dj, g.ci = ci + n1, g.cj = cj + n1, g.di = 0, g.dj = 0;
   g.batch = sD->batch;
   g.vecA = g.vecB = vec16_ok(sD, di + n1);
-  g.tma = tma_ok(sD);
+  g.tma = tma_ok(sD) && tma_ok(&T);
   g.tmaC = tma_ok(sC);
   g.skip = info;
-  if ((r = finish(run_syrk_ln(g, st)))) return r;
-  return potrf_run(m - n1, n - n1, sD, di + n1, dj + n1, sD, di + n1, dj + n1, info, 1, off + n1, st);
+  if ((r = finish(run_syrk_ln(g, st)))) return release(r);
+  if ((r = potrf_run(tm, tn, &T, 0, 0, sD, di + n1, dj + n1, info, 1, off + n1, st))) return release(r);
+  potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, false);
+  return release(finish(cudaGetLastError()));
 }
 
 int pb_dpotrf_l(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
@@ -400,6 +474,7 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
   w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
   w.stride = (int64_t)((m + 3) & ~3) * w.cn;
   double *wp = nullptr;
+  keep_pool_reserved();
   if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
   w.pA = wp;
   GemmArgs g;

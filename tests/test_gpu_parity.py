@@ -212,7 +212,7 @@ def spd_batch(rng, nb, n, shift=None):
 @pytest.mark.parametrize("mn", [(4, 4), (8, 8), (11, 11), (16, 16), (17, 17), (24, 24), (32, 32), (37, 37), (41, 41),
                                 (57, 57), (63, 63), (64, 64),
                                 (96, 96), (128, 128), (160, 160), (232, 232), (256, 256), (300, 300), (29, 13),
-                                (256, 128), (70, 33)])
+                                (256, 128), (70, 33), (320, 240), (300, 264)])
 def test_potrf_l_random_vs_oracle(mn):
     m, n = mn
     rng = np.random.default_rng(m * 7 + n)
@@ -236,7 +236,7 @@ def test_potrf_l_random_vs_oracle(mn):
         compare_storage(host(dD), D.storage, mask, m, f"potrf {mn} {oc}{od}")
 
 
-@pytest.mark.parametrize("n", [4, 8, 12, 16, 17, 24, 40, 57, 64, 128])
+@pytest.mark.parametrize("n", [4, 8, 12, 16, 17, 24, 40, 57, 64, 128, 256, 300])
 def test_potrf_failure_index_and_partial_writes(n):
     """Bad pivots: info equals the reference's index, and the failing item is
     written exactly as far as the reference writes it (ccore.pyx:884-899)."""
