@@ -1012,3 +1012,29 @@ def test_tma_pipeline_many_units_per_cta_beta1(op, m, n, k, nb):
         got, want = got[:, low], want[:, low]
     err = (torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)).item()
     assert err <= 50 * max(m, n, k) * EPS, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [260, 300])
+def test_syrk_potrf_large_failure_partial_writes(m):
+    """syrk_potrf_ln beyond one team (workspace + blocked potrf driver): items
+    failing in the first panel and in the trailing block get the reference's
+    row-panel partial writes (ccore.pyx:877-941); healthy items match."""
+    rng = np.random.default_rng(m)
+    k, nb = 16, 4
+    A = rand_batch(rng, nb, m, k)
+    C = O.HostBatch(nb, m, m)
+    g = rng.uniform(-1, 1, (m, m))
+    C.set_window(0, 0, np.broadcast_to(g @ g.T + m * np.eye(m), (nb, m, m)))
+    C.storage[1, O.element_offset(50, 50, C.cn)] = -1e6   # fails inside the first panel
+    C.storage[2, O.element_offset(m - 10, m - 10, C.cn)] = -1e6  # fails in the trailing block
+    D = rand_batch(rng, nb, m, m, fill=2.5)
+    dA, dC, dD = dev(A), dev(C), dev(D)
+    with pytest.raises(pb.NotPositiveDefiniteError) as ei:
+        level3.syrk_potrf_ln(m, k, dA, dA, dC, dD)
+    assert ei.value.index == 50 and ei.value.batch_index == 1
+    oinfo = O.syrk_potrf_ln(m, k, A, 0, 0, A, 0, 0, C, 0, 0, D, 0, 0)
+    assert list(oinfo) == [-1, 50, m - 10, -1]
+    mask = window_mask(D, (0, 0), m, m, lower=True)
+    mask[D.diag_off: D.diag_off + m] = True
+    compare_storage(host(dD), D.storage, mask, m, f"syrk_potrf {m} failure partial writes")
