@@ -390,6 +390,7 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
   };
   const Mat dm = to_mat(sD);
   potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, true);
+  note_launch();
   if ((r = potrf_run(m, n1, sC, ci, cj, sD, di, dj, info, merge, off, st))) return release(r);
   GemmArgs g;
   // trailing trapezoid: m - n1 rows, n - n1 columns (syrk tiles cover m - n1 columns, stores clip to g.n)
@@ -404,6 +405,7 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
   if ((r = finish(run_syrk_ln(g, st)))) return release(r);
   if ((r = potrf_run(tm, tn, &T, 0, 0, sD, di + n1, dj + n1, info, 1, off + n1, st))) return release(r);
   potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, false);
+  note_launch();
   return release(finish(cudaGetLastError()));
 }
 
