@@ -11,9 +11,10 @@ from . import fixtures, level3, pack
 from ._native import lib_path, load as load_native
 from .errors import (DimensionError, FactorizationError, MemoryLayoutError,
                      NotPositiveDefiniteError, PanelBlasError, SingularMatrixError)
-from .matstore import (ALIGN, PS, PanelBatch, SubRef, allocate_panel_batch,
-                       create_panel_batch, element_offset, memsize_panel_batch,
-                       memsize_panel_matrix)
+from .matstore import (ALIGN, PS, DenseVectorBatch, PanelBatch, SubRef, allocate_panel_batch,
+                       allocate_vector_batch, create_panel_batch, create_vector_batch, element_offset,
+                       memsize_panel_batch, memsize_panel_matrix, memsize_split_batch, memsize_vector,
+                       panel_data_elems)
 from .pack import ColBatch
 
 __version__ = "0.1.0"
@@ -25,9 +26,10 @@ def backend_name():
 
 
 __all__ = [
-    "ALIGN", "PS", "ColBatch", "PanelBatch", "SubRef", "allocate_panel_batch", "backend_name",
-    "create_panel_batch", "element_offset", "fixtures", "level3", "lib_path", "load_native",
-    "memsize_panel_batch", "memsize_panel_matrix", "pack",
+    "ALIGN", "PS", "ColBatch", "DenseVectorBatch", "PanelBatch", "SubRef", "allocate_panel_batch",
+    "allocate_vector_batch", "backend_name", "create_panel_batch", "create_vector_batch", "element_offset",
+    "fixtures", "level3", "lib_path", "load_native", "memsize_panel_batch", "memsize_panel_matrix",
+    "memsize_split_batch", "memsize_vector", "pack", "panel_data_elems",
     "DimensionError", "FactorizationError", "MemoryLayoutError", "NotPositiveDefiniteError",
     "PanelBlasError", "SingularMatrixError",
 ]

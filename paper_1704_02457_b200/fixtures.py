@@ -60,7 +60,7 @@ def _window(mat, b, ai, aj, m, n):
     n = mat.cols - aj if n is None else n
     if ai < 0 or aj < 0 or ai + m > mat.rows or aj + n > mat.cols or not 0 <= b < mat.batch:
         raise DimensionError(f"fixture window ({ai}:{ai + m}, {aj}:{aj + n}) of item {b} out of bounds")
-    row = mat.storage[b].detach().cpu().numpy()
+    row = mat.data[b].detach().cpu().numpy()
     return row[_offsets(ai, aj, m, n, mat.panel_length)]
 
 
@@ -77,9 +77,11 @@ def read_fixture(path, device="cuda"):
         arr = _read_array(fh)
     m, n = arr.shape
     out = allocate_panel_batch(1, m, n, device="cpu", zero=True)
-    row = out.storage[0].numpy()
+    row = out.data[0].numpy()
     row[_offsets(0, 0, m, n, out.panel_length)] = arr
-    return out if device == "cpu" else PanelBatch(1, m, n, out.storage.to(device))
+    if device == "cpu":
+        return out
+    return PanelBatch(1, m, n, out.storage.to(device), out.diag_storage.to(device))
 
 
 def write_ocp_fixture(path, nx, nu, stages, P):

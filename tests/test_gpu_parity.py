@@ -29,16 +29,51 @@ from paper_1704_02457_b200 import level3, pack  # noqa: E402
 EPS = np.finfo(np.float64).eps
 
 
+# Every test runs on both batch layouts (matstore.py): "split" (data plane +
+# diag plane, the default) and "interleaved" (the reference's item layout).
+LAYOUT = "split"
+_ORIG = {}  # id(PanelBatch) -> host storage it was made from (padding bytes of a split batch)
+
+
+@pytest.fixture(autouse=True, params=["split", "interleaved"])
+def layout(request):
+    global LAYOUT
+    LAYOUT = request.param
+    _ORIG.clear()
+    yield request.param
+    _ORIG.clear()
+
+
+def alloc(nb, m, n, zero=False):
+    return pb.allocate_panel_batch(nb, m, n, zero=zero, layout=LAYOUT)
+
+
 def dev(h):
-    """HostBatch -> PanelBatch on cuda:0 (same bytes)."""
-    t = torch.from_numpy(h.storage.copy()).cuda()
-    p = pb.create_panel_batch(h.batch, h.rows, h.cols, t)
+    """HostBatch -> PanelBatch on cuda:0 (same bytes) in the current layout."""
+    if LAYOUT == "interleaved":
+        t = torch.from_numpy(h.storage.copy()).cuda()
+        p = pb.create_panel_batch(h.batch, h.rows, h.cols, t)
+    else:
+        de, dn = pb.panel_data_elems(h.rows, h.cols), min(h.rows, h.cols)
+        data = torch.from_numpy(np.ascontiguousarray(h.storage[:, :de])).cuda()
+        diag = torch.from_numpy(np.ascontiguousarray(h.storage[:, h.diag_off: h.diag_off + dn])).cuda()
+        p = pb.create_panel_batch(h.batch, h.rows, h.cols, data.reshape(-1), diag.reshape(-1))
+        _ORIG[id(p)] = (p, h.storage.copy())
     p.diag_lo, p.diag_hi = h.diag_lo, h.diag_hi
     return p
 
 
 def host(p):
-    return p.storage.detach().cpu().numpy()
+    """Reference item layout of a device batch (numpy [batch, memsize/8])."""
+    st = p.item_storage().detach().cpu().numpy()
+    if p.layout == "split" and id(p) in _ORIG:  # padding slots as they were on the host
+        base = _ORIG[id(p)][1].copy()
+        de, dn = pb.panel_data_elems(p.rows, p.cols), min(p.rows, p.cols)
+        doff = p.memsize // 8 - (-(-dn * 8 // 64) * 8)
+        base[:, :de] = st[:, :de]
+        base[:, doff: doff + dn] = st[:, doff: doff + dn]
+        return base
+    return st
 
 
 def fp_close(got, want, n, what=""):
@@ -333,7 +368,7 @@ def test_gemm_special_cases_exact():
         dC = pack.panel_from_array(c)
         nanA = pack.panel_from_array(np.full((nb, m, k), np.nan))
         nanB = pack.panel_from_array(np.full((nb, n, k), np.nan))
-        dD = pb.allocate_panel_batch(nb, m, n, zero=True)
+        dD = alloc(nb, m, n, zero=True)
         level3.gemm_nt(m, n, k, 0.0, nanA, nanB, 1.0, dC, dD)  # alpha=0: A*B ignored even if NaN
         assert np.array_equal(pack.panel_to_array(dD).cpu().numpy(), c)
         level3.gemm_nt(m, n, k, 0.0, nanA, nanB, -2.0, dC, dD)
@@ -358,31 +393,31 @@ def test_aliasing_and_determinism_bit_exact():
         a = pack.panel_from_array(rng.uniform(-1, 1, (nb, m, k)))
         c = rng.uniform(-1, 1, (nb, m, m))
         alias = pack.panel_from_array(c)
-        sep = pb.allocate_panel_batch(nb, m, m, zero=True)
+        sep = alloc(nb, m, m, zero=True)
         level3.gemm_nt(m, m, k, 1.0, a, a, 0.5, alias, alias)
         level3.gemm_nt(m, m, k, 1.0, a, a, 0.5, pack.panel_from_array(c), sep)
         assert torch.equal(pack.panel_to_array(alias), pack.panel_to_array(sep))
         alias = pack.panel_from_array(c)
-        sep2 = pb.allocate_panel_batch(nb, m, m, zero=True)
+        sep2 = alloc(nb, m, m, zero=True)
         level3.syrk_ln(m, k, 1.0, a, a, 0.5, alias, alias)
         level3.syrk_ln(m, k, 1.0, a, a, 0.5, pack.panel_from_array(c), sep2)
         assert torch.equal(torch.tril(pack.panel_to_array(alias)), torch.tril(pack.panel_to_array(sep2)))
         s = spd_batch(rng, nb, m)
         inplace = pack.panel_from_array(s)
-        out = pb.allocate_panel_batch(nb, m, m, zero=True)
+        out = alloc(nb, m, m, zero=True)
         level3.potrf_l(m, inplace, inplace)
         level3.potrf_l(m, pack.panel_from_array(s), out)
         assert torch.equal(torch.tril(pack.panel_to_array(inplace)), torch.tril(pack.panel_to_array(out)))
         assert torch.equal(inplace.diag_inv, out.diag_inv)
         bm = pack.panel_from_array(rng.uniform(-1, 1, (nb, 7, m)))
-        x1 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        x1 = alloc(nb, 7, m, zero=True)
         level3.trsm_rltn(7, m, 1.0, out, bm, x1)
-        x2 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        x2 = alloc(nb, 7, m, zero=True)
         pack.gecp(7, m, bm, x2)
         level3.trsm_rltn(7, m, 1.0, out, x2, x2)  # D == B in place
         assert torch.equal(x1.storage, x2.storage)
         # determinism: same inputs, bit-identical outputs run to run
-        x3 = pb.allocate_panel_batch(nb, 7, m, zero=True)
+        x3 = alloc(nb, 7, m, zero=True)
         level3.trsm_rltn(7, m, 1.0, out, bm, x3)
         assert torch.equal(x1.storage, x3.storage)
 
@@ -393,7 +428,7 @@ def test_broadcast_operand():
     a = rng.uniform(-1, 1, (nb, m, k))
     b1 = rng.uniform(-1, 1, (1, n, k))
     dA, dB1 = pack.panel_from_array(a), pack.panel_from_array(b1)
-    dD = pb.allocate_panel_batch(nb, m, n, zero=True)
+    dD = alloc(nb, m, n, zero=True)
     level3.gemm_nt(m, n, k, 1.0, dA, dB1, 0.0, dD, dD)
     want = a @ b1[0].T
     assert O.rel_fro(pack.panel_to_array(dD).cpu().numpy(), want) < O.tol(k)
@@ -410,7 +445,7 @@ def test_pack_unpack_roundtrip_bit_exact():
         m, n = int(rng.integers(0, 40)), int(rng.integers(0, 40))
         ai, aj = int(rng.integers(0, 9)), int(rng.integers(0, 9))
         arr = rng.uniform(-1, 1, (nb, m, n))
-        big = pb.allocate_panel_batch(nb, ai + m + 3, aj + n + 3, zero=True)
+        big = alloc(nb, ai + m + 3, aj + n + 3, zero=True)
         src = pack.ColBatch.from_array(arr)
         pack.pack_matrix(src, m, n, big.ref(ai, aj))
         out = pack.ColBatch.from_array(np.zeros((nb, m, n)))
@@ -425,13 +460,13 @@ def test_pack_unpack_roundtrip_bit_exact():
         # row-major bridges
         back = pack.panel_to_array(big.ref(ai, aj), m, n).cpu().numpy()
         assert np.array_equal(back, arr)
-        big2 = pb.allocate_panel_batch(nb, ai + m + 3, aj + n + 3, zero=True)
+        big2 = alloc(nb, ai + m + 3, aj + n + 3, zero=True)
         pack.gecp(m, n, big.ref(ai, aj), big2.ref(ai, aj))
         assert torch.equal(big.storage, big2.storage)
 
 
 def test_pack_kat_element_46():
-    d = pb.allocate_panel_batch(2, 8, 8, zero=True)
+    d = alloc(2, 8, 8, zero=True)
     pack.pack_matrix(pack.ColBatch.from_array(np.full((2, 1, 1), 5.0)), 1, 1, d.ref(6, 3))
     assert torch.all(d.data[:, 46] == 5.0) and float(d.data.abs().sum()) == 10.0
 
@@ -444,21 +479,22 @@ def test_config1_full_batch_sampled():
     """C1: gemm_nt 64^3, alpha=beta=1, batch 4096 (BASELINE configs[0])."""
     nb, s = 4096, 64
     g = torch.Generator(device="cuda").manual_seed(1)
-    A, B, C = (pb.allocate_panel_batch(nb, s, s) for _ in range(3))
+    A, B, C = (alloc(nb, s, s) for _ in range(3))
     for x in (A, B, C):
         x.storage.uniform_(-1, 1, generator=g)
-    D = pb.allocate_panel_batch(nb, s, s, zero=True)
+    D = alloc(nb, s, s, zero=True)
     level3.gemm_nt(s, s, s, 1.0, A, B, 1.0, C, D)
     # linearity: gemm(2A) - 2 gemm(A) with beta=0 is exactly zero
-    D2 = pb.allocate_panel_batch(nb, s, s, zero=True)
-    A2 = pb.create_panel_batch(nb, s, s, A.storage * 2.0)
+    D2 = alloc(nb, s, s, zero=True)
+    A2 = pb.create_panel_batch(nb, s, s, A.storage * 2.0,
+                               None if A.diag_storage is None else A.diag_storage.clone())
     level3.gemm_nt(s, s, s, 1.0, A2, B, 0.0, C, D2)
-    D1 = pb.allocate_panel_batch(nb, s, s, zero=True)
+    D1 = alloc(nb, s, s, zero=True)
     level3.gemm_nt(s, s, s, 1.0, A, B, 0.0, C, D1)
     assert torch.equal(D2.data, 2.0 * D1.data)
     idx = np.random.default_rng(0).choice(nb, 12, replace=False)
     sub = torch.as_tensor(idx, device="cuda")
-    hA, hB, hC = (O.HostBatch(12, s, s, x.storage[sub].cpu().numpy()) for x in (A, B, C))
+    hA, hB, hC = (O.HostBatch(12, s, s, x.item_storage()[sub].cpu().numpy()) for x in (A, B, C))
     hD = O.HostBatch(12, s, s)
     O.gemm_nt(s, s, s, 1.0, hA, 0, 0, hB, 0, 0, 1.0, hC, 0, 0, hD, 0, 0)
     fp_close(D.data[sub].cpu().numpy(), hD.storage[:, : 64 * 64], s, "C1 sample")
@@ -472,7 +508,7 @@ def test_config2_potrf_large_batch_residual(n):
     M = torch.rand((nb, n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     a = M @ M.transpose(1, 2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
     C = pack.panel_from_array(a)
-    D = pb.allocate_panel_batch(nb, n, n, zero=True)
+    D = alloc(nb, n, n, zero=True)
     info = level3.potrf_l(n, C, D)
     assert int((info >= 0).sum()) == 0
     L = torch.tril(pack.panel_to_array(D))
@@ -481,7 +517,7 @@ def test_config2_potrf_large_batch_residual(n):
     dinv = D.diag_inv
     assert float((dinv * torch.diagonal(L, dim1=1, dim2=2) - 1).abs().max()) <= 4 * EPS
     idx = torch.as_tensor(np.random.default_rng(n).choice(nb, 8, replace=False), device="cuda")
-    hC = O.HostBatch(8, n, n, C.storage[idx].cpu().numpy())
+    hC = O.HostBatch(8, n, n, C.item_storage()[idx].cpu().numpy())
     hD = O.HostBatch(8, n, n)
     O.potrf_l(n, hC, 0, 0, hD, 0, 0)
     fp_close(torch.tril(L[idx]).cpu().numpy(), np.tril(hD.window(0, 0, n, n)), n, "C2 sample")
@@ -628,7 +664,7 @@ def test_getrf_reconstruction_and_edge_rules():
     nb, m = 8, 20
     a = rng.uniform(-1, 1, (nb, m, m))
     C = pack.panel_from_array(a)
-    D = pb.allocate_panel_batch(nb, m, m, zero=True)
+    D = alloc(nb, m, m, zero=True)
     ipiv = level3.getrf_pivot(m, m, C, D)
     lu = pack.panel_to_array(D).cpu().numpy()
     piv = ipiv.cpu().numpy()
@@ -643,7 +679,7 @@ def test_getrf_reconstruction_and_edge_rules():
     before = D.storage.clone()
     assert level3.getrf_pivot(0, m, C, D) is None and level3.getrf_nopivot(m, 0, C, D) is None
     assert torch.equal(before, D.storage)
-    big = pb.allocate_panel_batch(1, 200, 200, zero=True)
+    big = alloc(1, 200, 200, zero=True)
     with pytest.raises(RuntimeError):
         level3.getrf_pivot(200, 200, big, big)
 
@@ -992,12 +1028,12 @@ def test_tma_pipeline_many_units_per_cta_beta1(op, m, n, k, nb):
     C tile of consecutive units through shared rings): every item of a large
     batch against a dense fp64 torch reference, written window only."""
     g = torch.Generator(device="cuda").manual_seed(7)
-    A = pb.allocate_panel_batch(nb, m, k)
-    B = A if op == "syrk" else pb.allocate_panel_batch(nb, n, k)
-    C = pb.allocate_panel_batch(nb, m, n)
+    A = alloc(nb, m, k)
+    B = A if op == "syrk" else alloc(nb, n, k)
+    C = alloc(nb, m, n)
     for x in {id(x): x for x in (A, B, C)}.values():
         x.storage.uniform_(-1, 1, generator=g)
-    D = pb.allocate_panel_batch(nb, m, n)
+    D = alloc(nb, m, n)
     D.storage.fill_(-7.5)
     if op == "gemm":
         level3.gemm_nt(m, n, k, -0.5, A, B, 1.0, C, D)

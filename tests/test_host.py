@@ -40,21 +40,55 @@ def test_element_offset_injective_in_bounds():
 
 def test_panel_batch_views_on_cpu_storage():
     nb, m, n = 3, 6, 5
-    p = pb.allocate_panel_batch(nb, m, n, device="cpu", zero=True)
+    p = pb.allocate_panel_batch(nb, m, n, device="cpu", zero=True, layout="interleaved")
+    assert p.layout == "interleaved"
     assert p.storage.shape == (nb, memsize_panel_matrix(m, n) // 8)
     assert p.data.shape == (nb, 8 * 8)
     assert p.diag_inv.shape == (nb, 5)
     assert p.panels().shape == (nb, 2, 8, 4)
     p.panels()[1, 1, 3, 2] = 7.0  # row 6, col 3
     assert float(p.data[1, element_offset(6, 3, 4, 8)]) == 7.0
+    p.panels()[1, 1, 3, 1] = 5.0  # row 5, col 3
+    assert p.get(1, 5, 3) == 5.0
     d = p.descriptor()
     assert (d.m, d.n, d.cn, d.batch, d.stride) == (m, n, 8, nb, p.storage.shape[1])
     assert d.dA - d.pA == 64 * 8
     one = pb.allocate_panel_batch(1, m, n, device="cpu")
     bd = one.descriptor(7)
-    assert bd.batch == 7 and bd.stride == 0
+    assert bd.batch == 7 and bd.stride == 0 and bd.dA_stride == 0
     with pytest.raises(pb.DimensionError):
         p.descriptor(7)
+
+
+def test_split_layout_planes_and_item_storage():
+    nb, m, n = 3, 6, 5
+    p = pb.allocate_panel_batch(nb, m, n, device="cpu", zero=True)
+    assert p.layout == "split"
+    assert p.storage.shape == (nb, 8 * 8) and p.diag_storage.shape == (nb, 5)
+    d = p.descriptor()
+    assert (d.stride, d.dA_stride) == (64, 5)
+    assert d.dA == p.diag_storage.data_ptr()
+    p.set(2, 5, 4, 3.5)
+    p.diag_inv[2, 4] = 0.25
+    assert p.get(2, 5, 4) == 3.5
+    with pytest.raises(pb.DimensionError):
+        p.get(3, 0, 0)
+    with pytest.raises(pb.DimensionError):
+        p.set(0, 6, 0, 1.0)
+    # assembled reference layout == an interleaved batch holding the same values
+    q = pb.allocate_panel_batch(nb, m, n, device="cpu", zero=True, layout="interleaved")
+    q.set(2, 5, 4, 3.5)
+    q.diag_inv[2, 4] = 0.25
+    assert torch.equal(p.item_storage(), q.item_storage())
+    assert p.item_bytes(2).tobytes() == q.item_bytes(2).tobytes()
+    # shard views share memory
+    s = p.shard(1, 3)
+    assert s.batch == 2 and s.get(1, 5, 4) == 3.5 and s.descriptor().pA == p.descriptor().pA + 64 * 8
+    # n = 4 items are back to back: one 128-byte line each
+    four = pb.allocate_panel_batch(5, 4, 4, device="cpu")
+    assert four.descriptor().stride == 16 and four.descriptor().dA_stride == 4
+    assert pb.memsize_split_batch(5, 4, 4) == (5 * 128, 5 * 32)
+    assert pb.panel_data_elems(5, 3) == 32
 
 
 def test_create_panel_batch_validation():
@@ -63,8 +97,46 @@ def test_create_panel_batch_validation():
     buf = torch.zeros(100, dtype=torch.float64)
     q = pb.create_panel_batch(2, 4, 4, buf)
     assert q.storage.data_ptr() == buf.data_ptr()  # no copy, contents untouched
+    assert q.layout == "interleaved"
     with pytest.raises(pb.MemoryLayoutError):
         pb.create_panel_batch(1, 4, 4, torch.zeros(100, dtype=torch.float32))
+    # split: data plane + diag plane
+    data, diag = torch.zeros(2 * 16, dtype=torch.float64), torch.zeros(8, dtype=torch.float64)
+    s = pb.create_panel_batch(2, 4, 4, data, diag)
+    assert s.layout == "split" and s.diag_storage.data_ptr() == diag.data_ptr()
+    with pytest.raises(pb.MemoryLayoutError, match="diag plane"):
+        pb.create_panel_batch(2, 4, 4, data, torch.zeros(7, dtype=torch.float64))
+    with pytest.raises(pb.MemoryLayoutError, match="data plane"):
+        pb.create_panel_batch(2, 4, 4, torch.zeros(31, dtype=torch.float64), diag)
+    with pytest.raises(pb.MemoryLayoutError, match="aligned"):
+        pb.create_panel_batch(1, 4, 4, torch.zeros(40, dtype=torch.float64)[1:17], diag)
+
+
+def test_dense_vector_batch_kats():
+    # reference matstore.py:261-285, tests/test_matstore.py (memsize_vector)
+    assert pb.memsize_vector(0) == 0
+    assert pb.memsize_vector(1) == 64
+    assert pb.memsize_vector(8) == 64
+    assert pb.memsize_vector(9) == 128
+    with pytest.raises(pb.DimensionError):
+        pb.memsize_vector(-1)
+    v = pb.allocate_vector_batch(3, 5, device="cpu", zero=True)
+    assert v.data.shape == (3, 8) and v.memsize == 64 and v.stride == 8
+    v.set(2, 4, 1.5)
+    assert v.get(2, 4) == 1.5
+    with pytest.raises(pb.DimensionError):
+        v.get(2, 5)
+    assert v.to_array().shape == (3, 5)
+    buf = torch.arange(24, dtype=torch.float64)
+    w = pb.create_vector_batch(3, 5, buf)
+    assert w.data.data_ptr() == buf.data_ptr() and w.get(1, 0) == 8.0  # one 64-byte slot per item
+    with pytest.raises(pb.MemoryLayoutError, match="required"):
+        pb.create_vector_batch(4, 5, buf)
+    # diag_inv exposed as a vector batch view
+    p = pb.allocate_panel_batch(2, 6, 4, device="cpu", zero=True)
+    p.diag_inv[1, 3] = 2.0
+    dv = p.diag_vector()
+    assert dv.len == 4 and dv.get(1, 3) == 2.0
 
 
 def test_level3_bounds_errors_before_launch():
