@@ -23,13 +23,28 @@
  *                        kgetrf_panel, krowswap, lu_rowsolve_drv, gemm_nn_drv
  *
  * Conventions (mirroring the reference core):
- *   - caller owns every buffer; nothing here allocates device memory;
+ *   - caller owns every buffer; nothing here allocates device memory.  The
+ *     calls whose reference counterpart needs scratch (level3.py:59, 236,
+ *     338: unaligned windows, in-place trmm, the blocked factorization of
+ *     large windows) take a caller-owned device workspace `work` of
+ *     `work_bytes` bytes (256-byte aligned), sized by the matching
+ *     pb_*_worksize query on the same arguments (0 = none needed, NULL ok);
+ *     the library keeps no global state besides per-kernel launch
+ *     attributes, and never changes the device's memory pools;
  *   - all pointers are DEVICE pointers; work is enqueued on `stream`
  *     (a cudaStream_t, NULL = legacy default stream) and is asynchronous;
  *   - panel size ps = 4; element (i, j) of an item lives at
  *       (i - i%4)*cn + 4*j + i%4      (matstore.py:37-45)
- *   - windows may start anywhere (ai%4 != 0 included); writes never leave
- *     the m_store x n_store window (syrk/potrf: lower triangle only);
+ *   - windows may start anywhere (ai%4 != 0 included); results never leave
+ *     the m_store x n_store window (syrk/potrf: lower triangle only): every
+ *     byte outside it reads back unchanged after the call.  Stream contract:
+ *     the streaming kernels store whole 32-byte sectors, re-storing the
+ *     bytes of a sector that lie outside the window with the values they
+ *     read in the same kernel (strict upper of a diagonal 4x4 block, padding
+ *     rows of the last panel).  So, as for partial overlap below, another
+ *     stream must not write those sectors of the SAME item while the call
+ *     runs; disjoint items, and windows sharing no 32-byte sector, may be
+ *     processed concurrently on any streams;
  *   - D == C (gemm, syrk, potrf) and D == B (trsm) aliasing is supported;
  *     partial overlap is undefined (level3.py:14-15);
  *   - return 0 on success, -i if argument i (1-based) is invalid,
@@ -49,6 +64,7 @@ extern "C" {
 
 #define PB_PS 4
 #define PB_ERR_CUDA (-1000)
+#define PB_ERR_WORKSPACE (-1001) /* work smaller than the worksize query said */
 
 /* A batch of equally-shaped panel-major matrices: blasfeo_dmat
  * / panelblas PanelMatrix (matstore.py:68-115) with
@@ -65,7 +81,7 @@ typedef struct pb_dmat_batch {
   int64_t dA_stride; /* doubles between consecutive items' dA             */
 } pb_dmat_batch;
 
-/* ABI version (bumped on any signature change). */
+/* ABI version (bumped on any signature change): 2 = caller-owned workspace. */
 int pb_version(void);
 /* Human-readable text of the last error raised on this thread. */
 const char *pb_last_error(void);
@@ -97,11 +113,16 @@ int pb_dgemm_nn(int m, int n, int k, double alpha,
 
 /* D = alpha*B*A, A an n x n lower-triangular right factor (entries above
  * its diagonal are never read), B and D m x n (level3.py:140-153,
- * trmm_rlnn_drv ccore.pyx:834-852).  D = alpha*acc for every alpha. */
+ * trmm_rlnn_drv ccore.pyx:834-852).  D = alpha*acc for every alpha.
+ * Workspace: in place (D on B's storage) with n > 24. */
+int64_t pb_dtrmm_rlnn_worksize(int m, int n, const pb_dmat_batch *sA, int ai, int aj,
+                               const pb_dmat_batch *sB, int bi, int bj,
+                               const pb_dmat_batch *sD, int di, int dj);
 int pb_dtrmm_rlnn(int m, int n, double alpha,
                   const pb_dmat_batch *sA, int ai, int aj,
                   const pb_dmat_batch *sB, int bi, int bj,
-                  const pb_dmat_batch *sD, int di, int dj, void *stream);
+                  const pb_dmat_batch *sD, int di, int dj,
+                  void *work, int64_t work_bytes, void *stream);
 
 /* D * A^T = alpha*B, A n x n lower non-unit, B and D m x n
  * (blasfeo_dtrsm_rltn).  Reciprocals of A's diagonal: use_dA != 0 reuses
@@ -120,22 +141,34 @@ int pb_dtrsm_rltn(int m, int n, double alpha,
  * non-squared variant).  Writes sD->dA[dj .. dj+n) = 1/L[j,j].
  * info[b] = -1, or the first pivot index with d <= 0 (NaN passes, as in
  * ccore.pyx:423); a failing item is written exactly as far as the
- * reference would have written it before returning. */
+ * reference would have written it before returning (an unaligned D window,
+ * di % 4 != 0, of a failing item is left untouched, level3.py:338-344).
+ * Workspace: windows not factored by one kernel (n > 128, or tall windows
+ * that do not fit one CTA) and unaligned D windows of those. */
+int64_t pb_dpotrf_l_worksize(int m, int n,
+                             const pb_dmat_batch *sC, int ci, int cj,
+                             const pb_dmat_batch *sD, int di, int dj);
 int pb_dpotrf_l(int m, int n,
                 const pb_dmat_batch *sC, int ci, int cj,
                 const pb_dmat_batch *sD, int di, int dj,
-                int32_t *info, void *stream);
+                int32_t *info, void *work, int64_t work_bytes, void *stream);
 
 /* D = chol(lower(C + A*B^T)), m x n with n <= m, A m x k, B n x k
- * (level3.py:353-391, syrk_potrf_drv ccore.pyx:908-941): the product goes
- * to a stream-ordered workspace, then pb_dpotrf_l's rules apply to it
- * (info, diag_inv, partial writes of a failed item). */
+ * (level3.py:353-391, syrk_potrf_drv ccore.pyx:908-941): fused in one
+ * kernel when the item fits one CTA, else the product goes to workspace
+ * and pb_dpotrf_l's rules apply to it (info, diag_inv, partial writes of a
+ * failed item). */
+int64_t pb_dsyrk_potrf_ln_worksize(int m, int n, int k,
+                                   const pb_dmat_batch *sA, int ai, int aj,
+                                   const pb_dmat_batch *sB, int bi, int bj,
+                                   const pb_dmat_batch *sC, int ci, int cj,
+                                   const pb_dmat_batch *sD, int di, int dj);
 int pb_dsyrk_potrf_ln(int m, int n, int k,
                       const pb_dmat_batch *sA, int ai, int aj,
                       const pb_dmat_batch *sB, int bi, int bj,
                       const pb_dmat_batch *sC, int ci, int cj,
                       const pb_dmat_batch *sD, int di, int dj,
-                      int32_t *info, void *stream);
+                      int32_t *info, void *work, int64_t work_bytes, void *stream);
 
 /* LU of the m x n window of C into D (level3.getrf_pivot / getrf_nopivot,
  * level3.py:405-498): D holds unit-L below the diagonal and U on/above,

@@ -31,6 +31,7 @@ class DmatBatch(ctypes.Structure):
     ]
 
 
+ABI_VERSION = 2
 P = ctypes.POINTER(DmatBatch)
 _i, _d, _v, _l = ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64
 
@@ -42,15 +43,18 @@ SIGNATURES = {
     "pb_dgemm_nt": (_i, [_i, _i, _i, _d, P, _i, _i, P, _i, _i, _d, P, _i, _i, P, _i, _i, _v]),
     "pb_dsyrk_ln": (_i, [_i, _i, _d, P, _i, _i, P, _i, _i, _d, P, _i, _i, P, _i, _i, _v]),
     "pb_dtrsm_rltn": (_i, [_i, _i, _d, P, _i, _i, _i, P, _i, _i, P, _i, _i, _v, _v]),
-    "pb_dpotrf_l": (_i, [_i, _i, P, _i, _i, P, _i, _i, _v, _v]),
+    "pb_dpotrf_l": (_i, [_i, _i, P, _i, _i, P, _i, _i, _v, _v, _l, _v]),
+    "pb_dpotrf_l_worksize": (_l, [_i, _i, P, _i, _i, P, _i, _i]),
     "pb_dpack_cm": (_i, [_i, _i, _v, _l, _l, P, _i, _i, _v]),
     "pb_dunpack_cm": (_i, [_i, _i, P, _i, _i, _v, _l, _l, _v]),
     "pb_dpack": (_i, [_i, _i, _v, _l, _l, _l, P, _i, _i, _v]),
     "pb_dunpack": (_i, [_i, _i, P, _i, _i, _v, _l, _l, _l, _v]),
     "pb_dgecp": (_i, [_i, _i, P, _i, _i, P, _i, _i, _v]),
     "pb_dgemm_nn": (_i, [_i, _i, _i, _d, P, _i, _i, P, _i, _i, _d, P, _i, _i, P, _i, _i, _v]),
-    "pb_dtrmm_rlnn": (_i, [_i, _i, _d, P, _i, _i, P, _i, _i, P, _i, _i, _v]),
-    "pb_dsyrk_potrf_ln": (_i, [_i, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, _v, _v]),
+    "pb_dtrmm_rlnn": (_i, [_i, _i, _d, P, _i, _i, P, _i, _i, P, _i, _i, _v, _l, _v]),
+    "pb_dtrmm_rlnn_worksize": (_l, [_i, _i, P, _i, _i, P, _i, _i, P, _i, _i]),
+    "pb_dsyrk_potrf_ln": (_i, [_i, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, _v, _v, _l, _v]),
+    "pb_dsyrk_potrf_ln_worksize": (_l, [_i, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i, P, _i, _i]),
     "pb_driccati_chain": (_i, [_i, _i, _i, P, P, P, P, _v, _v]),
     "pb_dgetrf": (_i, [_i, _i, P, _i, _i, P, _i, _i, _i, _v, _l, _v, _v]),
 }
@@ -76,7 +80,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.pb_version() != 1:
+        if lib.pb_version() != ABI_VERSION:
             raise RuntimeError("libpb_b200.so ABI version mismatch")
     except Exception as exc:  # no fallback: remember and re-raise loudly
         _load_error = exc
@@ -93,6 +97,30 @@ def call(name, *args):
         msg = lib.pb_last_error().decode(errors="replace")
         raise RuntimeError(f"{name} failed with status {st}: {msg}")
     return st
+
+
+def worksize(name, *args):
+    """Bytes of caller-owned workspace ``name`` needs for these arguments
+    (its ``<name>_worksize`` query); raises like :func:`call` on a bad argument."""
+    lib = load()
+    v = getattr(lib, name + "_worksize")(*args)
+    if v < 0:
+        msg = lib.pb_last_error().decode(errors="replace")
+        raise RuntimeError(f"{name}_worksize failed with status {v}: {msg}")
+    return int(v)
+
+
+def workspace(nbytes, device):
+    """A device workspace of ``nbytes`` from PyTorch's caching allocator on
+    the current stream (the reference's L3 allocates its scratch the same
+    way, level3.py:59, 236, 338): (tensor-or-None, pointer, bytes)."""
+    if nbytes <= 0:
+        return None, ctypes.c_void_p(0), 0
+    import torch
+    t = torch.empty((nbytes + 255) // 8 + 32, dtype=torch.float64, device=device)
+    base = t.data_ptr()
+    shift = (-base) % 256
+    return t, ctypes.c_void_p(base + shift), nbytes
 
 
 def launch_count(reset=False):

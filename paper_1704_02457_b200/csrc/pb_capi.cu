@@ -68,19 +68,35 @@ static bool tma_ok(const pb_dmat_batch *x) { return ((uintptr_t)x->pA & 15) == 0
 
 static int finish(cudaError_t e) { return e == cudaSuccess ? 0 : cuda_fail(e); }
 
-// The device's default stream-ordered pool would otherwise return its pages
-// at every synchronize (release threshold 0) and re-map them on the next
-// call's cudaMallocAsync -- milliseconds per GB of scratch.
-static void keep_pool_reserved() {
-  static thread_local int done_dev = -1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+static int work_fail() {
+  t_err = "workspace smaller than the worksize query reported";
+  return PB_ERR_WORKSPACE;
+}
+
+static size_t ws_round(size_t b) { return (b + 255) & ~(size_t)255; }
+static size_t panel_bytes(int64_t rows, int64_t cols) {
+  return ws_round(sizeof(double) * (size_t)((rows + 3) & ~3) * (size_t)((cols + 3) & ~3));
+}
+
+// caller-owned workspace, carved by a bump pointer in call order
+struct Work {
+  char *base = nullptr;
+  size_t cap = 0, used = 0;
+  double *take(size_t bytes) {
+    const size_t a = ws_round(used);
+    if (a + bytes > cap) return nullptr;
+    used = a + bytes;
+    return (double *)(base + a);
   }
-  done_dev = dev;
+};
+
+static pb_dmat_batch panel_desc(double *p, int rows, int cols, int batch, double *dA = nullptr,
+                                int64_t dA_stride = 0) {
+  pb_dmat_batch w;
+  memset(&w, 0, sizeof w);
+  w.pA = p, w.dA = dA, w.m = rows, w.n = cols, w.cn = (cols + 3) & ~3, w.batch = batch;
+  w.stride = (int64_t)((rows + 3) & ~3) * w.cn, w.dA_stride = dA_stride;
+  return w;
 }
 
 }  // namespace pb
@@ -89,7 +105,7 @@ using namespace pb;
 
 extern "C" {
 
-int pb_version(void) { return 1; }
+int pb_version(void) { return 2; }
 const char *pb_last_error(void) { return t_err.c_str(); }
 // diag_inv of an output holds min(m, n) reciprocals of its matrix; a factor
 // of width w written at column dj needs dj + w of them.  The reference core
@@ -183,8 +199,8 @@ int pb_dgemm_nn(int m, int n, int k, double alpha, const pb_dmat_batch *sA, int 
   return gemm_common(2, m, n, k, alpha, sA, ai, aj, sB, bi, bj, beta, sC, ci, cj, sD, di, dj, stream, nullptr);
 }
 
-int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
-                  int bj, const pb_dmat_batch *sD, int di, int dj, void *stream) {
+static int trmm_check(int m, int n, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi, int bj,
+                      const pb_dmat_batch *sD, int di, int dj) {
   // positions: m1 n2 alpha3 A4 ai5 aj6 B7 bi8 bj9 D10 di11 dj12 (level3.py:140-153)
   if (m < 0) return fail_arg(1, "negative size");
   if (n < 0) return fail_arg(2, "negative size");
@@ -193,36 +209,49 @@ int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
   int r;
   if ((r = check_mat(sA, 4, ai, aj, n, n, batch, false))) return r;
   if ((r = check_mat(sB, 7, bi, bj, m, n, batch, false))) return r;
-  if ((r = check_mat(sD, 10, di, dj, m, n, batch, true))) return r;
+  return check_mat(sD, 10, di, dj, m, n, batch, true);
+}
+
+// In place (D on B's storage, test_level3.py:190-195): tiles of D would
+// overwrite columns of B other column tiles still read once n spans several
+// tiles, so B's window is first copied to workspace (one warp-tile spans all
+// n <= 24 columns: no copy needed).
+static size_t trmm_ws(int m, int n, const pb_dmat_batch *sB, const pb_dmat_batch *sD) {
+  return (sD->pA == sB->pA && n > 24) ? panel_bytes(m, n) * sD->batch : 0;
+}
+
+int64_t pb_dtrmm_rlnn_worksize(int m, int n, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                               int bj, const pb_dmat_batch *sD, int di, int dj) {
+  const int r = trmm_check(m, n, sA, ai, aj, sB, bi, bj, sD, di, dj);
+  if (r) return r;
+  if (m == 0 || n == 0 || sD->batch == 0) return 0;
+  return (int64_t)trmm_ws(m, n, sB, sD);
+}
+
+int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                  int bj, const pb_dmat_batch *sD, int di, int dj, void *work, int64_t work_bytes, void *stream) {
+  // positions: m1 n2 alpha3 A4 ai5 aj6 B7 bi8 bj9 D10 di11 dj12 work13 work_bytes14
+  int r;
+  if ((r = trmm_check(m, n, sA, ai, aj, sB, bi, bj, sD, di, dj))) return r;
+  const int batch = sD->batch;
   if (m == 0 || n == 0 || batch == 0) return 0;  // level3.py:148-149
+  const size_t need = trmm_ws(m, n, sB, sD);
+  if (need && (!work || work_bytes < (int64_t)need)) return fail_arg(13, "workspace too small (see pb_dtrmm_rlnn_worksize)");
   // D = alpha * X * T as an NN product: the streamed operand X (= B) is the
   // kernel's A, the triangular factor T (= A) its B
   cudaStream_t st = (cudaStream_t)stream;
-  // In place (D on B's storage, test_level3.py:190-195): tiles of D would
-  // overwrite columns of B other column tiles still read once n spans
-  // several tiles, so B's window is first copied to a stream-ordered
-  // workspace (one warp-tile spans all n <= 24 columns: no copy needed).
   pb_dmat_batch w;
-  double *wp = nullptr;
   const pb_dmat_batch *sX = sB;
   int xi = bi, xj = bj;
-  if (sD->pA == sB->pA && n > 24) {
-    memset(&w, 0, sizeof w);
-    w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
-    w.stride = (int64_t)((m + 3) & ~3) * w.cn;
-    keep_pool_reserved();
-    if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
-    w.pA = wp;
+  if (need) {
+    w = panel_desc((double *)work, m, n, batch);
     CopyArgs c;
     memset(&c, 0, sizeof c);
     c.m = m, c.n = n;
     c.S = to_mat(sB), c.D = to_mat(&w);
     c.si = bi, c.sj = bj;
     c.batch = batch;
-    if ((r = finish(run_gecp(c, st)))) {
-      cudaFreeAsync(wp, st);
-      return r;
-    }
+    if ((r = finish(run_gecp(c, st)))) return r;
     sX = &w, xi = 0, xj = 0;
   }
   GemmArgs g;
@@ -236,12 +265,7 @@ int pb_dtrmm_rlnn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
   g.tma = tma_ok(sA) && tma_ok(sX);
   g.tmaC = false;
   g.skip = nullptr;
-  r = finish(run_trmm_rlnn(g, st));
-  if (wp) {
-    const int rf = finish(cudaFreeAsync(wp, st));
-    if (!r) r = rf;
-  }
-  return r;
+  return finish(run_trmm_rlnn(g, st));
 }
 
 int pb_dsyrk_ln(int m, int k, double alpha, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
@@ -315,121 +339,202 @@ int pb_dtrsm_rltn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
 }
 
 // ---- potrf_l ------------------------------------------------------------
+//
+// Direct kernels: square n <= 16 (register / quad, bit-exact), 17..64 (one
+// warp per item), 65..128 (one CTA per item, register tiles), tall windows
+// that fit one team's shared memory (team kernel).  Everything else runs the
+// blocked driver below, on caller-owned workspace (the library never
+// allocates):
+//   1. square factor of the first n1 <= 128 columns into D (direct kernel);
+//   2. rows [n1, m):  W = C21 L11^{-T}   (trsm, reciprocals reused) -> workspace;
+//   3. trailing:      T = C22 - W W^T     (syrk, lower trapezoid)   -> workspace;
+//      potrf of T into D22 (recursive, failing items skipped, global index);
+//   4. commit W -> D21: all rows of a healthy item; for an item failing at
+//      pivot f >= n1 the rows above f's row panel and the panel itself
+//      (rows < (f & ~3) + 4), which is exactly what the reference's row-panel
+//      order (ccore.pyx:877-905) has written when it stops; nothing for f < n1.
+// An unaligned D window (di % 4 != 0) factors into an aligned workspace copy
+// and commits the lower trapezoid of healthy items only: level3.potrf_l
+// factors into scratch and copies on success (level3.py:338-344), while the
+// core writes diag_inv directly (so does this path).
 
-// Blocked-driver failure fix-up.  The reference factors row panel by row
-// panel (ccore.pyx:877-905): an item failing in row panel p leaves D's rows
-// past p untouched.  The blocked driver writes the whole tall panel first,
-// so it snapshots D's rows [n1, m) x cols [0, n1) and, for items that then
-// fail in the trailing block, puts back the rows below the failing row panel.
-// save = true: S <- D for every item; save = false: D <- S where needed.
-__global__ void potrf_blk_snapshot(Mat D, ix di, ix dj, ix m, ix n1, double *S, const int32_t *info, int off,
-                                   bool save) {
-  const ix b = blockIdx.x;
-  ix r0 = n1;
-  if (!save) {
-    const int f = info[b] - off;
-    if (info[b] < 0 || f < n1) return;  // healthy, or failed before / inside the panel (panel kernel's writes)
-    r0 = (ix)(f / 4) * 4 + 4;           // reference writes row panel f/4 (off-diagonal blocks), nothing below
+static bool potrf_direct(int m, int n) {
+  if (m == n) return n <= 128;
+  return n <= 232 && potrf_fits(m, n);
+}
+static int potrf_split(int n) {  // first panel width of the blocked driver
+  int n1 = ((n / 2) + 7) / 8 * 8;
+  return n1 > 128 ? 128 : (n1 < 8 ? 8 : n1);
+}
+
+static size_t potrf_ws(int m, int n, int di, int batch) {
+  if (potrf_direct(m, n)) return 0;
+  if (di & 3) return panel_bytes(m, n) * batch + potrf_ws(m, n, 0, batch);
+  const int n1 = m == n || n > 128 ? potrf_split(n) : n;
+  size_t w = 0;
+  if (m > n1) w += panel_bytes(m - n1, n1) * batch;
+  if (n > n1) w += panel_bytes(m - n1, n - n1) * batch + potrf_ws(m - n1, n - n1, 0, batch);
+  return w;
+}
+
+// rows of W (relative rows [0, rows)) item b may commit into D, see step 4
+__global__ void potrf_commit_kernel(Mat S, Mat D, ix di, ix dj, ix rows, ix cols, const int32_t *info, int off,
+                                    int n1, int lower) {
+  const ix b = blockIdx.y;
+  const int f = info[b];
+  ix rmax;
+  if (lower) {
+    rmax = f < 0 ? rows : 0;  // unaligned window: healthy items only
+  } else if (f < 0) {
+    rmax = rows;
+  } else {
+    const ix fr = (ix)f - off;  // window-relative failing pivot
+    rmax = fr >= n1 ? ((fr & ~(ix)3) + 4) - n1 : 0;
+    if (rmax > rows) rmax = rows;
   }
+  if (rmax <= 0) return;
+  const double *s = S.p + b * S.stride;
   double *d = D.p + b * D.stride;
-  double *sv = S + b * (m - n1) * n1;
-  // storage order (row quad, column, row in quad): consecutive threads touch
-  // consecutive doubles of a panel when di is panel-aligned
-  const ix q0 = r0 / 4, nq = (m + 3) / 4;
-  for (ix e = threadIdx.x; e < (nq - q0) * n1 * 4; e += blockDim.x) {
-    const ix r = (q0 + e / (4 * n1)) * 4 + (e & 3), c = (e >> 2) % n1;
-    if (r >= m) continue;
-    double *pd = d + eo(di + r, dj + c, D.cn);
-    double *ps = sv + (r - n1) * n1 + c;
-    if (save) *ps = *pd;
-    else *pd = *ps;
+  // consecutive threads walk the source panel-major order (4 rows x column)
+  const ix nq = (rmax + 3) / 4, per = nq * cols * 4;
+  for (ix e = (ix)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (ix)gridDim.x * blockDim.x) {
+    const ix r = (e / (4 * cols)) * 4 + (e & 3), c = (e >> 2) % cols;
+    if (r >= rmax || (lower && c > r)) continue;
+    d[eo(di + r, dj + c, D.cn)] = s[eo(r, c, S.cn)];
   }
 }
 
+static int potrf_commit(const pb_dmat_batch &W, const pb_dmat_batch *sD, int di, int dj, int rows, int cols,
+                        int32_t *info, int off, int n1, int lower, cudaStream_t st) {
+  const int batch = sD->batch;
+  ix per = (ix)((rows + 3) / 4) * cols * 4;
+  unsigned gx = (unsigned)((per + 255) / 256);
+  if (gx > 64) gx = 64;
+  if (gx < 1) gx = 1;
+  for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
+    const int nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    Mat S = to_mat(&W), D = to_mat(sD);
+    S.p += (ix)b0 * S.stride;
+    D.p += (ix)b0 * D.stride;
+    potrf_commit_kernel<<<dim3(gx, (unsigned)nb), 256, 0, st>>>(S, D, di, dj, rows, cols, info + b0, off, n1, lower);
+    note_launch();
+  }
+  return finish(cudaGetLastError());
+}
+
 static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
-                     int32_t *info, int merge, int off, cudaStream_t st) {
-  // PB_POTRF_BLOCK=b splits any n >= 2b into a b-column panel + syrk + trailing factor (0 = only when the
-  // item does not fit one team); default 128 (n=256: 2.27 -> 2.18 ms, profiles/r01_potrf_blocked_failfix.txt)
-  static const int blk = getenv("PB_POTRF_BLOCK") ? atoi(getenv("PB_POTRF_BLOCK")) : 128;
-  const bool split = blk >= 8 && blk % 8 == 0 && n >= 2 * blk && potrf_fits(m, blk);
-  if (!split && potrf_fits(m, n)) {
+                     int32_t *info, int merge, int off, Work &w, cudaStream_t st) {
+  const int batch = sD->batch;
+  if (potrf_direct(m, n)) {
     PotrfArgs g;
     g.m = m, g.n = n;
     g.C = to_mat(sC), g.D = to_mat(sD);
     g.ci = ci, g.cj = cj, g.di = di, g.dj = dj;
     g.info = info;
-    g.batch = sD->batch;
+    g.batch = batch;
     g.merge = merge;
     g.info_offset = off;
     return finish(run_potrf_l(g, st));
   }
-  // blocked: tall panel factor of the first n1 columns, syrk downdate of
-  // the trailing block, recursive factor of the trailing block.
-  int n1 = 8;
-  while (n1 + 8 < n && potrf_fits(m, n1 + 8)) n1 += 8;
-  if (split) n1 = blk;
   int r;
-  const int batch = sD->batch;
-  // trailing-block downdate goes to scratch T (not D) so a failing item's D
-  // keeps its bytes past the failure; snapshot of D's panel rows below n1
-  const int tm = m - n1, tn = n - n1;
-  pb_dmat_batch T{};
-  T.m = tm, T.n = tn, T.cn = (tn + 3) / 4 * 4, T.batch = batch;
-  T.stride = (int64_t)((tm + 3) / 4 * 4) * T.cn;
-  double *snap = nullptr;
-  keep_pool_reserved();
-  if ((r = finish(cudaMallocAsync((void **)&T.pA, sizeof(double) * (size_t)T.stride * batch, st)))) return r;
-  if ((r = finish(cudaMallocAsync((void **)&snap, sizeof(double) * (size_t)tm * n1 * batch, st)))) {
-    cudaFreeAsync(T.pA, st);
-    return r;
+  if (di & 3) {
+    // aligned workspace copy of the window; diag_inv straight into D's
+    double *p = w.take(panel_bytes(m, n) * batch);
+    if (!p) return work_fail();
+    pb_dmat_batch X = panel_desc(p, m, n, batch, sD->dA ? sD->dA + dj : nullptr, sD->dA_stride);
+    if ((r = potrf_run(m, n, sC, ci, cj, &X, 0, 0, info, merge, off, w, st))) return r;
+    return potrf_commit(X, sD, di, dj, m, n, info, off, 0, 1, st);
   }
-  auto release = [&](int rc) {
-    cudaFreeAsync(T.pA, st);
-    cudaFreeAsync(snap, st);
-    return rc;
-  };
-  const Mat dm = to_mat(sD);
-  potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, true);
-  note_launch();
-  if ((r = potrf_run(m, n1, sC, ci, cj, sD, di, dj, info, merge, off, st))) return release(r);
-  GemmArgs g;
-  // trailing trapezoid: m - n1 rows, n - n1 columns (syrk tiles cover m - n1 columns, stores clip to g.n)
-  g.m = m - n1, g.n = n - n1, g.k = n1, g.alpha = -1.0, g.beta = 1.0;
-  g.A = to_mat(sD), g.B = to_mat(sD), g.C = to_mat(sC), g.D = to_mat(&T);
-  g.ai = di + n1, g.aj = dj, g.bi = di + n1, g.bj = dj, g.ci = ci + n1, g.cj = cj + n1, g.di = 0, g.dj = 0;
-  g.batch = sD->batch;
-  g.vecA = g.vecB = vec16_ok(sD, di + n1);
-  g.tma = tma_ok(sD) && tma_ok(&T);
-  g.tmaC = tma_ok(sC);
-  g.skip = info;
-  if ((r = finish(run_syrk_ln(g, st)))) return release(r);
-  if ((r = potrf_run(tm, tn, &T, 0, 0, sD, di + n1, dj + n1, info, 1, off + n1, st))) return release(r);
-  potrf_blk_snapshot<<<batch, 256, 0, st>>>(dm, di, dj, m, n1, snap, info, off, false);
-  note_launch();
-  return release(finish(cudaGetLastError()));
+  const int n1 = m == n || n > 128 ? potrf_split(n) : n;
+  // 1. square factor of the first n1 columns
+  if ((r = potrf_run(n1, n1, sC, ci, cj, sD, di, dj, info, merge, off, w, st))) return r;
+  if (m == n1) return 0;
+  // 2. rows below against it, into workspace
+  double *pw = w.take(panel_bytes(m - n1, n1) * batch);
+  if (!pw) return work_fail();
+  pb_dmat_batch W = panel_desc(pw, m - n1, n1, batch);
+  {
+    TrsmArgs g;
+    g.m = m - n1, g.n = n1, g.alpha = 1.0;
+    g.A = to_mat(sD), g.B = to_mat(sC), g.D = to_mat(&W);
+    g.ai = di, g.aj = dj, g.bi = ci + n1, g.bj = cj, g.di = 0, g.dj = 0;
+    g.use_dA = 1;
+    g.info = nullptr;
+    g.batch = batch;
+    g.skip = info;
+    if ((r = trsm_fits(m - n1, n1) ? finish(run_trsm_rltn(g, st)) : fail_arg(2, "panel too wide"))) return r;
+  }
+  // 3. trailing block: T = C22 - W W^T, factored into D22
+  if (n > n1) {
+    double *pt = w.take(panel_bytes(m - n1, n - n1) * batch);
+    if (!pt) return work_fail();
+    pb_dmat_batch T = panel_desc(pt, m - n1, n - n1, batch);
+    GemmArgs g;
+    // lower trapezoid: m - n1 rows, n - n1 columns (syrk tiles cover m - n1 columns, stores clip to g.n)
+    g.m = m - n1, g.n = n - n1, g.k = n1, g.alpha = -1.0, g.beta = 1.0;
+    g.A = to_mat(&W), g.B = to_mat(&W), g.C = to_mat(sC), g.D = to_mat(&T);
+    g.ai = 0, g.aj = 0, g.bi = 0, g.bj = 0, g.ci = ci + n1, g.cj = cj + n1, g.di = 0, g.dj = 0;
+    g.batch = batch;
+    g.vecA = g.vecB = true;
+    g.tma = true;
+    g.tmaC = tma_ok(sC);
+    g.skip = info;
+    if ((r = finish(run_syrk_ln(g, st)))) return r;
+    if ((r = potrf_run(m - n1, n - n1, &T, 0, 0, sD, di + n1, dj + n1, info, 1, off + n1, w, st))) return r;
+  }
+  // 4. commit the rows below the first panel
+  return potrf_commit(W, sD, di + n1, dj, m - n1, n1, info, off, n1, 0, st);
+}
+
+static int potrf_check(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
+                       int dj, int pc, int pd) {
+  if (m < 0) return fail_arg(1, "negative size");
+  if (n < 0 || n > m) return fail_arg(2, "potrf_l needs 0 <= n <= m");
+  if (!sD) return fail_arg(pd, "null matrix descriptor");
+  int r;
+  if ((r = check_mat(sC, pc, ci, cj, m, n, sD->batch, false))) return r;
+  if ((r = check_mat(sD, pd, di, dj, m, n, sD->batch, true))) return r;
+  if (n == 0 || sD->batch == 0) return 0;
+  if (!sD->dA) return fail_arg(pd, "output needs diag_inv storage");
+  return check_dinv(sD, pd, dj, n);
+}
+
+int64_t pb_dpotrf_l_worksize(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
+                             int dj) {
+  const int r = potrf_check(m, n, sC, ci, cj, sD, di, dj, 3, 6);
+  if (r) return r;
+  if (n == 0 || sD->batch == 0) return 0;
+  return (int64_t)potrf_ws(m, n, di, sD->batch);
 }
 
 int pb_dpotrf_l(int m, int n, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
-                int32_t *info, void *stream) {
-  // positions: m1 n2 C3 ci4 cj5 D6 di7 dj8 info9
-  if (m < 0) return fail_arg(1, "negative size");
-  if (n < 0 || n > m) return fail_arg(2, "potrf_l needs 0 <= n <= m");
-  if (!sD) return fail_arg(6, "null matrix descriptor");
-  const int batch = sD->batch;
+                int32_t *info, void *work, int64_t work_bytes, void *stream) {
+  // positions: m1 n2 C3 ci4 cj5 D6 di7 dj8 info9 work10 work_bytes11
   int r;
-  if ((r = check_mat(sC, 3, ci, cj, m, n, batch, false))) return r;
-  if ((r = check_mat(sD, 6, di, dj, m, n, batch, true))) return r;
-  if (n == 0 || batch == 0) return 0;  // level3.py:335-336
-  if (!sD->dA) return fail_arg(6, "output needs diag_inv storage");
-  if ((r = check_dinv(sD, 6, dj, n))) return r;
+  if ((r = potrf_check(m, n, sC, ci, cj, sD, di, dj, 3, 6))) return r;
+  if (n == 0 || sD->batch == 0) return 0;  // level3.py:335-336
   if (!info) return fail_arg(9, "info is required");
-  return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, (cudaStream_t)stream);
+  const size_t need = potrf_ws(m, n, di, sD->batch);
+  if (need && (!work || work_bytes < (int64_t)need)) return fail_arg(10, "workspace too small (see pb_dpotrf_l_worksize)");
+  Work w;
+  w.base = (char *)work, w.cap = (size_t)(work ? work_bytes : 0);
+  return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, w, (cudaStream_t)stream);
 }
 
-int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
-                      int bj, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
-                      int32_t *info, void *stream) {
-  // positions: m1 n2 k3 A4 ai5 aj6 B7 bi8 bj9 C10 ci11 cj12 D13 di14 dj15 info16 (level3.py:353-391)
+// ---- syrk_potrf_ln --------------------------------------------------------
+
+static bool syrk_potrf_fused(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
+                             int bi, int bj, const pb_dmat_batch *sD, int di, bool &ab_same) {
+  ab_same = sA->pA == sB->pA && sA->stride == sB->stride && sA->cn == sB->cn && ai == bi && aj == bj;
+  // squares the register-resident small potrf covers keep its rounding
+  // (zero factors then reproduce potrf_l bit for bit, test_level3.py:632-641)
+  const bool small = m == n && n <= 16 && (di & 3) == 0 && tma_ok(sD);
+  return !small && syrk_potrf_fits(m, n, k, ab_same);
+}
+
+static int syrk_potrf_check(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
+                            int bi, int bj, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di,
+                            int dj) {
   if (m < 0) return fail_arg(1, "negative size");
   if (n < 0 || n > m) return fail_arg(2, "syrk_potrf_ln needs 0 <= n <= m");
   if (k < 0) return fail_arg(3, "negative size");
@@ -440,18 +545,49 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
   if ((r = check_mat(sB, 7, bi, bj, n, k, batch, false))) return r;
   if ((r = check_mat(sC, 10, ci, cj, m, n, batch, false))) return r;
   if ((r = check_mat(sD, 13, di, dj, m, n, batch, true))) return r;
-  if (n == 0 || batch == 0) return 0;  // level3.py:370-371
+  if (n == 0 || batch == 0) return 0;
   if (!sD->dA) return fail_arg(13, "output needs diag_inv storage");
-  if ((r = check_dinv(sD, 13, dj, n))) return r;
+  return check_dinv(sD, 13, dj, n);
+}
+
+static size_t syrk_potrf_ws(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
+                            int bi, int bj, const pb_dmat_batch *sD, int di) {
+  const int batch = sD->batch;
+  if (k == 0) return potrf_ws(m, n, di, batch);
+  bool ab_same;
+  if (syrk_potrf_fused(m, n, k, sA, ai, aj, sB, bi, bj, sD, di, ab_same)) return 0;
+  return panel_bytes(m, n) * batch + potrf_ws(m, n, di, batch);
+}
+
+int64_t pb_dsyrk_potrf_ln_worksize(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj,
+                                   const pb_dmat_batch *sB, int bi, int bj, const pb_dmat_batch *sC, int ci, int cj,
+                                   const pb_dmat_batch *sD, int di, int dj) {
+  const int r = syrk_potrf_check(m, n, k, sA, ai, aj, sB, bi, bj, sC, ci, cj, sD, di, dj);
+  if (r) return r;
+  if (n == 0 || sD->batch == 0) return 0;
+  return (int64_t)syrk_potrf_ws(m, n, k, sA, ai, aj, sB, bi, bj, sD, di);
+}
+
+int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB, int bi,
+                      int bj, const pb_dmat_batch *sC, int ci, int cj, const pb_dmat_batch *sD, int di, int dj,
+                      int32_t *info, void *work, int64_t work_bytes, void *stream) {
+  // positions: m1 n2 k3 A4 ai5 aj6 B7 bi8 bj9 C10 ci11 cj12 D13 di14 dj15 info16 work17 work_bytes18
+  // (level3.py:353-391)
+  int r;
+  if ((r = syrk_potrf_check(m, n, k, sA, ai, aj, sB, bi, bj, sC, ci, cj, sD, di, dj))) return r;
+  const int batch = sD->batch;
+  if (n == 0 || batch == 0) return 0;  // level3.py:370-371
   if (!info) return fail_arg(16, "info is required");
+  const size_t need = syrk_potrf_ws(m, n, k, sA, ai, aj, sB, bi, bj, sD, di);
+  if (need && (!work || work_bytes < (int64_t)need))
+    return fail_arg(17, "workspace too small (see pb_dsyrk_potrf_ln_worksize)");
+  Work w;
+  w.base = (char *)work, w.cap = (size_t)(work ? work_bytes : 0);
   cudaStream_t st = (cudaStream_t)stream;
   // k == 0: exactly potrf_l of C (test_level3.py:343-353)
-  if (k == 0) return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, st);
-  const bool ab_same = sA->pA == sB->pA && sA->stride == sB->stride && sA->cn == sB->cn && ai == bi && aj == bj;
-  // squares the register-resident small potrf covers keep its rounding
-  // (zero factors then reproduce potrf_l bit for bit, test_level3.py:632-641)
-  const bool small = m == n && n <= 16 && (di & 3) == 0 && tma_ok(sD);
-  if (!small && syrk_potrf_fits(m, n, k, ab_same)) {
+  if (k == 0) return potrf_run(m, n, sC, ci, cj, sD, di, dj, info, 0, 0, w, st);
+  bool ab_same;
+  if (syrk_potrf_fused(m, n, k, sA, ai, aj, sB, bi, bj, sD, di, ab_same)) {
     // one fused kernel: the item's C tri, A and B windows in shared memory
     PotrfArgs g;
     g.m = m, g.n = n;
@@ -467,21 +603,16 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
     g.ai = ai, g.aj = aj, g.bi = bi, g.bj = bj, g.k = k;
     return finish(run_syrk_potrf(g, st));
   }
-  // W = lower trapezoid of C + A*B^T in a stream-ordered workspace, then
-  // potrf_l(W -> D).  syrk_potrf_drv (ccore.pyx:908-941) walks the same
-  // block rows as potrf_drv with the tile input C + A*B^T, so D's contents
-  // on a failed pivot follow potrf_l's rule on W.
-  pb_dmat_batch w;
-  memset(&w, 0, sizeof w);
-  w.m = m, w.n = n, w.cn = (n + 3) & ~3, w.batch = batch;
-  w.stride = (int64_t)((m + 3) & ~3) * w.cn;
-  double *wp = nullptr;
-  keep_pool_reserved();
-  if ((r = finish(cudaMallocAsync((void **)&wp, sizeof(double) * (size_t)w.stride * batch, st)))) return r;
-  w.pA = wp;
+  // W = lower trapezoid of C + A*B^T in workspace, then potrf_l(W -> D).
+  // syrk_potrf_drv (ccore.pyx:908-941) walks the same block rows as
+  // potrf_drv with the tile input C + A*B^T, so D's contents on a failed
+  // pivot follow potrf_l's rule on W.
+  double *wp = w.take(panel_bytes(m, n) * batch);
+  if (!wp) return work_fail();
+  pb_dmat_batch W = panel_desc(wp, m, n, batch);
   GemmArgs g;
   g.n = n, g.k = k, g.alpha = 1.0, g.beta = 1.0;
-  g.A = to_mat(sA), g.B = to_mat(sB), g.C = to_mat(sC), g.D = to_mat(&w);
+  g.A = to_mat(sA), g.B = to_mat(sB), g.C = to_mat(sC), g.D = to_mat(&W);
   g.batch = batch;
   g.tma = tma_ok(sA) && tma_ok(sB);
   g.tmaC = tma_ok(sC);
@@ -497,9 +628,8 @@ int pb_dsyrk_potrf_ln(int m, int n, int k, const pb_dmat_batch *sA, int ai, int 
     g.vecA = vec16_ok(sA, ai + n);
     r = finish(run_gemm_nt(g, st));
   }
-  if (!r) r = potrf_run(m, n, &w, 0, 0, sD, di, dj, info, 0, 0, st);
-  const int rf = finish(cudaFreeAsync(wp, st));
-  return r ? r : rf;
+  if (!r) r = potrf_run(m, n, &W, 0, 0, sD, di, dj, info, 0, 0, w, st);
+  return r;
 }
 
 // ---- pack / unpack / gecp ------------------------------------------------

@@ -255,12 +255,8 @@ static cudaError_t launch_chain(const ChainArgs &g, cudaStream_t st) {
   auto kern = chain_kernel<NXB, TW>;
   const int teams = 128 / (32 * TW);
   const size_t smem = sizeof(double) * Cfg::TEAM * teams;
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
-    if (occ < 1) occ = 1;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, 128, smem);
   ix grid = (g.batch + teams - 1) / teams;
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;
@@ -276,13 +272,7 @@ cudaError_t run_chain_riccati(const ChainArgs &g, int nx, int nu, cudaStream_t s
     case 8: return launch_chain<1, 2>(g, st);
     case 16: return launch_chain<2, 2>(g, st);
     case 24: return launch_chain<3, 2>(g, st);
-    case 32: {
-      // 4 warps per problem measured best (1.405 -> 1.321 ms at C5), PB_CHAIN_TW for A/B runs
-      static const int tw = getenv("PB_CHAIN_TW") ? atoi(getenv("PB_CHAIN_TW")) : 4;
-      if (tw == 1) return launch_chain<4, 1>(g, st);
-      if (tw == 4) return launch_chain<4, 4>(g, st);
-      return launch_chain<4, 2>(g, st);
-    }
+    case 32: return launch_chain<4, 4>(g, st);  // 4 warps per problem measured best (1.405 -> 1.321 ms at C5)
     case 48: return launch_chain<6, 4>(g, st);
     case 64: return launch_chain<8, 4>(g, st);
     default: return cudaErrorInvalidValue;

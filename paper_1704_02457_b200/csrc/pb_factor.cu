@@ -562,10 +562,8 @@ static cudaError_t launch_potrf(const PotrfArgs &g, cudaStream_t st) {
   int threads;
   size_t smem;
   const int teams = pick_teams(TW, team_elems, threads, smem);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-  if (occ < 1) occ = 1;
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, threads, smem);
   ix grid = (g.batch + teams - 1) / teams;
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;
@@ -585,9 +583,8 @@ bool potrf_fits(ix m, ix n) {
 }
 
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
-  static const bool team_only = getenv("PB_POTRF_TEAM") != nullptr;  // A/B switch
-  if (!team_only && potrf_reg_ok(g)) return run_potrf_reg(g, st);
   if (potrf_small_ok(g)) return run_potrf_small(g, st);
+  if (potrf_reg_ok(g)) return run_potrf_reg(g, st);
   const ix gm = (g.m + 7) / 8;
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
   const ix gn = (g.n + 7) / 8;
@@ -612,8 +609,7 @@ bool syrk_potrf_fits(ix m, ix n, ix k, bool ab_same) {
 
 // fused syrk + potrf: single-buffered generic team shapes
 cudaError_t run_syrk_potrf(const PotrfArgs &g, cudaStream_t st) {
-  static const bool team_only = getenv("PB_POTRF_TEAM") != nullptr;
-  if (!team_only && potrf_reg_ok(g)) return run_potrf_reg(g, st);
+  if (potrf_reg_ok(g)) return run_potrf_reg(g, st);
   const ix gm = (g.m + 7) / 8;
   if (gm <= 2) return launch_potrf<1, 2, false, 0, 0, true, 4>(g, st);
   if (gm <= 4) return launch_potrf<1, 4, false, 0, 0, true, 4>(g, st);
@@ -639,10 +635,8 @@ static cudaError_t launch_trsm(const TrsmArgs &g, cudaStream_t st) {
   int threads;
   size_t smem;
   const int teams = pick_teams(TW, team_elems, threads, smem);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-  if (occ < 1) occ = 1;
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, threads, smem);
   ix grid = (g.batch + teams - 1) / teams;
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;

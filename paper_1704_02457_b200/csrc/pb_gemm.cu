@@ -452,8 +452,11 @@ __global__ void __launch_bounds__(TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>::N
         const int cb = (int)(ul % (CB > 0 ? CB : 1));
         if (ul >= CB) mbar_wait(&cempty[cb], (unsigned)(((ul / (CB > 0 ? CB : 1)) - 1) & 1));
         const ix rc = g.ci + tm * BM;
-        const ix rows = min((ix)BM, g.m - tm * BM), cols = min((ix)BN, ncols - tn * BN);
-        const int npc = (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1);
+        // C columns clip at g.n, not at the syrk tile range: a lower trapezoid
+        // (g.n < g.m, the blocked potrf's trailing update) must not read past
+        // C's window (the consumers read only in-store elements of the tile)
+        const ix rows = min((ix)BM, g.m - tm * BM), cols = max((ix)0, min((ix)BN, g.n - tn * BN));
+        const int npc = cols > 0 ? (int)(((rc + rows - 1) >> 2) - (rc >> 2) + 1) : 0;
         const unsigned bytes = 32u * (unsigned)cols;
         if (lane == 0) mbar_arrive_expect_tx(&cfull[cb], bytes * npc);
         __syncwarp();
@@ -715,12 +718,8 @@ template <int KMAX, bool SYRK, int STG = 1>
 static cudaError_t launch_item(const GemmArgs &g, cudaStream_t st) {
   using Cfg = ItemCfg<KMAX, STG>;
   auto kern = gemm_item_kernel<KMAX, SYRK, STG>;
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTH, Cfg::SMEM);
-    if (occ < 1) occ = 1;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, Cfg::NTH, Cfg::SMEM);
   const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
   ix grid = (ix)num_sms() * occ;
   if (grid > rounds) grid = rounds;
@@ -821,15 +820,17 @@ static cudaError_t launch_item_reg(const GemmArgs &g, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // host dispatch
 
-static int g_num_sms = 0;
+static int g_num_sms[64] = {0};
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!g_num_sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_num_sms[dev] = v > 0 ? v : 148;
   }
-  return g_num_sms;
+  return g_num_sms[dev];
 }
 
 template <int MT, int NT, bool SYRK, int BOP = BOP_NT>
@@ -844,9 +845,7 @@ static cudaError_t launch_direct(const GemmArgs &g, cudaStream_t st) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // min 3 CTAs/SM (<= 85 registers): C3 n = 8..24 6.25 -> 4.63 ms summed (n = 16 alone 9 % slower)
-  static const int lb = getenv("PB_DIRECT_LB") ? atoi(getenv("PB_DIRECT_LB")) : 3;  // A/B switch
-  if (lb == 3) gemm_direct_kernel<MT, NT, SYRK, BOP, 3><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
-  else gemm_direct_kernel<MT, NT, SYRK, BOP, 1><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
+  gemm_direct_kernel<MT, NT, SYRK, BOP, 3><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
   note_launch();
   return cudaGetLastError();
 }
@@ -866,14 +865,8 @@ template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK>
 static cudaError_t launch_tiled(const GemmArgs &g, cudaStream_t st) {
   using Cfg = TiledCfg<BM, BN, WM, WN, KC, STAGES>;
   auto kern = gemm_tiled_kernel<BM, BN, WM, WN, KC, STAGES, SYRK>;
-  static bool configured = false;
-  static int occ = 1;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
-    if (occ < 1) occ = 1;
-    configured = true;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, Cfg::NTHREADS, Cfg::SMEM);
   const ix tiles_m = (g.m + BM - 1) / BM;
   const ix tiles_n = SYRK ? tiles_m : (g.n + BN - 1) / BN;
   const ix per = SYRK ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
@@ -890,14 +883,8 @@ template <int BM, int BN, int WM, int WN, int KC, int STAGES, bool SYRK, int CB 
 static cudaError_t launch_tma(const GemmArgs &g, cudaStream_t st) {
   using Cfg = TmaCfg<BM, BN, WM, WN, KC, STAGES, CB, BOP>;
   auto kern = gemm_tma_kernel<BM, BN, WM, WN, KC, STAGES, SYRK, CB, BOP>;
-  static bool configured = false;
-  static int occ = 1;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
-    if (occ < 1) occ = 1;
-    configured = true;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, Cfg::NTHREADS, Cfg::SMEM);
   const ix tiles_m = (g.m + BM - 1) / BM;
   const ix tiles_n = SYRK ? tiles_m : (g.n + BN - 1) / BN;
   const ix per = SYRK ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
@@ -920,11 +907,9 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
                          ((uintptr_t)g.D.p & 15) == 0 && (g.D.stride & 1) == 0;
   if (big <= 4 && one_panel) {
     // (k <= 4 only: the per-thread staging of larger k does not fit shared memory)
-    static const int item_stg = getenv("PB_ITEM_STG") ? atoi(getenv("PB_ITEM_STG")) : 1;  // A/B switch
-    // register-direct kernel (C3 n = 4: 3.40 -> 3.01 ms; capping it at 4-6 CTAs/SM spills and is slower)
-    static const int item_reg = getenv("PB_ITEM_REG") ? atoi(getenv("PB_ITEM_REG")) : 1;  // A/B switch
-    if (g.k <= 4 && item_reg) return launch_item_reg<SYRK>(g, st);
-    if (g.k <= 4) return item_stg == 2 ? launch_item<4, SYRK, 2>(g, st) : launch_item<4, SYRK, 1>(g, st);
+    // register-direct kernel (C3 n = 4: 3.40 -> 3.01 ms over the staged one;
+    // capping it at 4-6 CTAs/SM spills and is slower)
+    if (g.k <= 4) return launch_item_reg<SYRK>(g, st);
   }
   if (big <= 24) return dispatch_direct<SYRK>(g, st);
   const ix small = g.m < ncols ? g.m : ncols;
@@ -944,17 +929,8 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
       const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t) * wcost[i];
       if (area < best * 0.999) best = area, T = t;
     }
-    static const int force_t = getenv("PB_GEMM_T") ? atoi(getenv("PB_GEMM_T")) : 0;  // tuning sweeps
-    if (force_t) T = force_t;
     const bool k40 = g.k > 32 && g.k <= 40;
     const bool cs = g.beta != 0.0 && g.tmaC;  // C tile through shared memory
-    static const char *tcfg = getenv("PB_TMA_CS");  // A/B switch for the beta != 0 pipeline shape
-    if (tcfg && cs && T == 64 && !k40) {
-      const std::string v(tcfg);
-      if (v == "k16s4") return launch_tma<64, 64, 32, 16, 16, 4, SYRK, 1>(g, st);
-      if (v == "k16s3") return launch_tma<64, 64, 32, 16, 16, 3, SYRK, 1>(g, st);
-      if (v == "k8s6") return launch_tma<64, 64, 32, 16, 8, 6, SYRK, 1>(g, st);
-    }
 #define PB_TMA(T_, WM_, WN_, K_)                                                    \
   if (T == T_ && (K_ == 40) == k40) {                                                \
     if (cs) return launch_tma<T_, T_, WM_, WN_, K_, 2, SYRK, 1>(g, st);              \

@@ -1,5 +1,7 @@
 // Internal launch-argument structs shared by the kernels and the C ABI.
 #pragma once
+#include <mutex>
+
 #include "pb_common.cuh"
 
 namespace pb {
@@ -58,7 +60,36 @@ struct CopyArgs {
 };
 
 void note_launch();
-int num_sms();
+int num_sms();  // of the current device (cached per device)
+
+// Launch attributes of one kernel instantiation whose dynamic shared memory
+// depends on the call's shape: the max-dynamic-smem attribute is raised once
+// per device to the largest size seen and the occupancy is queried once per
+// (device, smem, threads) -- no per-call driver queries on the launch path.
+struct LaunchCache {
+  std::mutex mu;
+  int smem_set[16] = {0};
+  int64_t keys[64];
+  int vals[64];
+  int n = 0;
+  int occupancy(const void *kern, int threads, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 16 && (int)smem > smem_set[dev]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_set[dev] = (int)smem;
+    }
+    const int64_t key = ((int64_t)dev << 48) | ((int64_t)smem << 12) | threads;
+    for (int i = 0; i < n; ++i)
+      if (keys[i] == key) return vals[i];
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    if (occ < 1) occ = 1;
+    if (n < 64) keys[n] = key, vals[n++] = occ;
+    return occ;
+  }
+};
 
 cudaError_t run_gemm_nt(const GemmArgs &g, cudaStream_t st);
 cudaError_t run_syrk_ln(const GemmArgs &g, cudaStream_t st);
@@ -77,6 +108,7 @@ bool potrf_small_ok(const PotrfArgs &g);
 bool potrf_reg_ok(const PotrfArgs &g);
 cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
+cudaError_t run_potrf_exact_fixup(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
 size_t getrf_smem(int m, int n);
 cudaError_t run_getrf(int m, int n, int pivot, const Mat &C, ix ci, ix cj, const Mat &D, ix di, ix dj, int64_t *ipiv,

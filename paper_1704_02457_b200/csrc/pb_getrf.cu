@@ -203,10 +203,8 @@ cudaError_t run_getrf(int m, int n, int pivot, const Mat &C, ix ci, ix cj, const
   g.ld = m | 1;
   const size_t smem = getrf_smem(m, n);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(getrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, getrf_kernel, 32, smem);
-  if (occ < 1) occ = 1;
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)getrf_kernel, 32, smem);
   ix grid = (ix)num_sms() * occ;
   if (grid > batch) grid = batch;
   if (grid < 1) grid = 1;

@@ -26,8 +26,7 @@
 //  * no shared memory and no barriers: occupancy is set by registers only,
 //    and other warps hide each item's load latency and pivot chain; the
 //    next item's rows are prefetched into L2 by one bulk prefetch.
-#include <cstdlib>
-
+#include "pb_exact.cuh"
 #include "pb_gemm.cuh"
 
 namespace pb {
@@ -80,6 +79,7 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
     offD[i] = eo(g.di + 8 * i + r, g.dj + 2 * q, g.D.cn);
   }
   for (ix b = (ix)blockIdx.x; b < g.batch; b += nw) {
+    if (g.merge && g.info[b] >= 0) continue;  // blocked driver: item failed in an earlier panel
     const double *Cb = g.C.p + b * g.C.stride;
     if (pf_ok == 2 && lane < np4 && b + nw < g.batch)
       prefetch_l2(g.C.p + (b + nw) * g.C.stride + eo(g.ci + 4 * lane, g.cj, g.C.cn), pf_bytes);
@@ -118,6 +118,9 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
     }
     int fail = -1;
     double *dA = g.D.d + b * g.D.dstride + g.dj;
+    double dkeep[GM];
+#pragma unroll
+    for (int k = 0; k < GM; ++k) dkeep[k] = 0.0;
     // Control flow stays warp-uniform and branch-free: a failing pivot only
     // records its index and zeroes its reciprocal (the columns left of it
     // are final in a right-looking sweep and are never touched again; the
@@ -166,12 +169,7 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
           T[ti(i, k)][1] *= s1;
         }
       }
-      // reciprocals of the completed columns (the reference writes dinv
-      // column by column, also ahead of a failing pivot)
-      {
-        const int c = 8 * k + lane;
-        if (lane < 8 && c < n && (fail < 0 || c < fail)) dA[c] = myinv;
-      }
+      dkeep[k] = myinv;  // lane j < 8: 1/L[8k+j][8k+j], written after the finiteness check
       // trailing update  T(i,jj) -= P(i) P(jj)^T,  k < jj <= i
       if (k + 1 < GM) {
         double a0[GM], a1[GM];
@@ -194,11 +192,35 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
         }
       }
     }
-    if (lane == 0 && g.info) g.info[b] = fail;
     // write set: lower triangle of the window; a failing item only rows
     // < iif plus block row iif left of iif (iif = fail & ~3), as the
-    // reference stores before returning (ccore.pyx:884-899)
+    // reference stores before returning (ccore.pyx:884-899), and nothing of
+    // an unaligned window (level3.py:338-344 factors into scratch)
     const int iif = fail >= 0 ? (fail & ~3) : 0;
+    const bool none = fail >= 0 && (g.di & 3) != 0;
+    // A NaN / Inf among the results (a non-finite input, or overflow): the
+    // masked-multiplier updates may have spread it over more entries of its
+    // row than the reference does.  The item is left untouched here and
+    // marked (info = PB_INFO_EXACT); potrf_exact_kernel redoes it in the
+    // reference's own operation order right after this launch (pb_exact.cu).
+    // Detection is one FMA per register (x * 0 is NaN only for NaN / Inf x);
+    // a failing item's unused trailing entries count too (rare, still exact).
+    double chk = 0.0;
+#pragma unroll
+    for (int k = 0; k < GM; ++k) chk = fma(dkeep[k], 0.0, chk);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) chk = fma(T[t][1], 0.0, fma(T[t][0], 0.0, chk));
+    const bool nonfinite = !isfinite(chk);
+    if (!SYRK && __any_sync(FULL, nonfinite)) {
+      if (lane == 0) g.info[b] = PB_INFO_EXACT;
+      continue;
+    }
+    if (lane == 0 && g.info) g.info[b] = fail >= 0 ? fail + g.info_offset : -1;
+#pragma unroll
+    for (int k = 0; k < GM; ++k) {
+      const int c = 8 * k + lane;
+      if (lane < 8 && c < n && (fail < 0 || c < fail)) dA[c] = dkeep[k];
+    }
     double *Db = g.D.p + b * g.D.stride;
 #pragma unroll
     for (int i = 0; i < GM; ++i)
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int R = 8 * i + r, Cc = 8 * j + 2 * q + e;
-          bool w = R < n && Cc <= R;
+          bool w = R < n && Cc <= R && !none;
           if (fail >= 0) w = w && (R < iif || (R < iif + 4 && Cc < iif));
           if (w) Db[offD[i] + 4 * (8 * j + e)] = T[ti(i, j)][e];
         }
@@ -226,8 +248,8 @@ cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
   ix grid = (ix)num_sms() * occ;
   if (grid > ctas) grid = ctas;
   if (grid < 1) grid = 1;
-  static const int pf_mode = getenv("PB_REG_PF") ? atoi(getenv("PB_REG_PF")) : 1;  // A/B: 0 none, 1 panels, 2 prefixes
-  const int pf_ok = ((g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0) ? pf_mode : 0;
+  // next-item L2 prefetch of whole panels (measured best; profiles/r01_c2_kernels_ncu.txt)
+  const int pf_ok = ((g.ci & 3) == 0 && ((uintptr_t)g.C.p & 15) == 0 && (g.C.stride & 1) == 0) ? 1 : 0;
   kern<<<(unsigned)grid, 32, 0, st>>>(g, pf_ok);
   note_launch();
   return cudaGetLastError();
@@ -235,13 +257,10 @@ cudaError_t launch_reg(const PotrfArgs &g, cudaStream_t st) {
 
 }  // namespace
 
-// 9 <= n <= 16 stays on the bit-exact quad kernel unless PB_POTRF_REG16 is set (A/B runs)
-bool potrf_reg_ok(const PotrfArgs &g) {
-  static const int lo = getenv("PB_POTRF_REG16") ? 9 : 17;
-  return g.m == g.n && g.n >= lo && g.n <= 64 && !g.merge;
-}
+// 9 <= n <= 16 stays on the bit-exact quad kernel (aligned windows)
+bool potrf_reg_ok(const PotrfArgs &g) { return g.m == g.n && g.n >= 17 && g.n <= 64; }
 
-cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
+static cudaError_t run_potrf_reg_only(const PotrfArgs &g, cudaStream_t st) {
   const int gm = (int)((g.n + 7) / 8);
   if (g.syrk) {
     switch (gm) {
@@ -265,6 +284,12 @@ cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
     case 8: return launch_reg<8, false>(g, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st) {
+  const cudaError_t e = run_potrf_reg_only(g, st);
+  if (e != cudaSuccess || g.syrk) return e;
+  return run_potrf_exact_fixup(g, st);  // items marked PB_INFO_EXACT (non-finite), if any
 }
 
 }  // namespace pb

@@ -21,9 +21,6 @@
 // in-tile updates, IEEE sqrt and division, no FMA contraction -- so the
 // factor and diag_inv are bit-identical to the reference's.  Failure
 // index and the partially written factor of a failing item match too.
-#include <cstdlib>
-#include <string>
-
 #include "pb_gemm.cuh"
 
 namespace pb {
@@ -622,12 +619,8 @@ template <int N, int NTH = 128, int STG = 2, int MINB = 1>
 static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH, STG>;
   auto kern = potrf_small1_kernel<N, NTH, STG, MINB>;
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTH, Cfg::SMEM);
-    if (occ < 1) occ = 1;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, NTH, Cfg::SMEM);
   const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
   ix grid = (ix)num_sms() * occ;
   if (grid > rounds) grid = rounds;
@@ -641,12 +634,8 @@ template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
   auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB>;
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NTHREADS, Cfg::SMEM);
-    if (occ < 1) occ = 1;
-  }
+  static LaunchCache cache;
+  const int occ = cache.occupancy((const void *)kern, Cfg::NTHREADS, Cfg::SMEM);
   const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
   ix grid = (ix)num_sms() * occ;
   if (grid > rounds) grid = rounds;
@@ -666,33 +655,6 @@ static cudaError_t launch_small_default(const PotrfArgs &g, cudaStream_t st) {
   else return launch_small<N>(g, st);
 }
 
-// tuning hook for the benchmark sweeps (PB_SMALL_CFG = <threads>x<stages>)
-template <int N>
-static cudaError_t launch_small_tuned(const PotrfArgs &g, cudaStream_t st) {
-  const char *e = getenv("PB_SMALL_CFG");
-  if (e) {
-    const std::string v(e);
-    if (v == "64x2") return launch_small<N, 64, 2>(g, st);
-    if (v == "64x3") return launch_small<N, 64, 3>(g, st);
-    if (v == "128x3") return launch_small<N, 128, 3>(g, st);
-    if (v == "256x2") return launch_small<N, 256, 2>(g, st);
-    if (v == "64x4") return launch_small<N, 64, 4>(g, st);
-    if (v == "128x1") return launch_small<N, 128, 1>(g, st);
-    if (v == "64x1") return launch_small<N, 64, 1>(g, st);
-    if (v == "256x1") return launch_small<N, 256, 1>(g, st);
-    if (v == "128x1m4") return launch_small<N, 128, 1, false, 4>(g, st);
-    if (v == "128x1m3") return launch_small<N, 128, 1, false, 3>(g, st);
-    if (v == "64x2m5") return launch_small<N, 64, 2, false, 5>(g, st);
-    if (v == "64x1m8") return launch_small<N, 64, 1, false, 8>(g, st);
-    if (v == "256x1m2") return launch_small<N, 256, 1, false, 2>(g, st);
-    if (v == "32x1m16") return launch_small<N, 32, 1, false, 16>(g, st);
-    if (v == "64x2m6") return launch_small<N, 64, 2, false, 6>(g, st);
-    if (v == "32x2m12") return launch_small<N, 32, 2, false, 12>(g, st);
-  }
-  if (getenv("PB_QUAD_RMW")) return launch_small<N, 128, 2, true>(g, st);
-  return launch_small_default<N>(g, st);
-}
-
 bool potrf_small_ok(const PotrfArgs &g) {
   if (g.m != g.n || g.n > 16 || g.n < 1 || g.merge) return false;
   if ((g.ci & 3) || (g.di & 3)) return false;
@@ -702,55 +664,23 @@ bool potrf_small_ok(const PotrfArgs &g) {
 }
 
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
-  static const bool legacy = getenv("PB_SMALL_LEGACY") != nullptr;  // A/B switch for the sweeps
   // n <= 8: thread-per-item factor with whole-sector stores (potrf_small1_kernel):
-  // measured n = 4 0.27 -> 0.33, n = 8 0.34 -> 0.45 of HBM (profiles/r01_potrf_small_rmw.txt)
-  if (!legacy && g.n <= 8) {
-    switch (g.n) {
-      case 1: return launch_small1<1>(g, st);
-      case 2: return launch_small1<2>(g, st);
-      case 3: return launch_small1<3>(g, st);
-      case 4: {
-        const char *e = getenv("PB_SMALL_CFG");
-        if (e) {
-          const std::string v(e);
-          if (v == "64x1m8") return launch_small1<4, 64, 1, 8>(g, st);
-          if (v == "128x1m4") return launch_small1<4, 128, 1, 4>(g, st);
-          if (v == "128x2m3") return launch_small1<4, 128, 2, 3>(g, st);
-          if (v == "128x2") return launch_small1<4>(g, st);
-        }
-        // single stage, 16 warps/SM: 71.8 -> 68.9 ms at the C2 n = 4 point
-        return launch_small1<4, 128, 1, 4>(g, st);
-      }
-      case 5: return launch_small1<5>(g, st);
-      case 6: return launch_small1<6>(g, st);
-      case 7: return launch_small1<7>(g, st);
-      case 8: {
-        const char *e = getenv("PB_SMALL_CFG");
-        if (e) {
-          const std::string v(e);
-          if (v == "64x1m8") return launch_small1<8, 64, 1, 8>(g, st);
-          if (v == "64x1m6") return launch_small1<8, 64, 1, 6>(g, st);
-          if (v == "32x1m14") return launch_small1<8, 32, 1, 14>(g, st);
-          if (v == "64x2") return launch_small1<8, 64, 2>(g, st);
-        }
-        return launch_small1<8>(g, st);
-      }
-    }
-  }
+  // measured n = 4 0.27 -> 0.33, n = 8 0.34 -> 0.45 of HBM (profiles/r01_potrf_small_rmw.txt);
+  // n = 4 single stage, 16 warps/SM: 71.8 -> 68.9 ms at the C2 n = 4 point
   switch (g.n) {
+    case 1: return launch_small1<1>(g, st);
+    case 2: return launch_small1<2>(g, st);
+    case 3: return launch_small1<3>(g, st);
+    case 4: return launch_small1<4, 128, 1, 4>(g, st);
+    case 5: return launch_small1<5>(g, st);
+    case 6: return launch_small1<6>(g, st);
+    case 7: return launch_small1<7>(g, st);
+    case 8: return launch_small1<8>(g, st);
 #define PB_SMALL(N_) \
   case N_:           \
     return launch_small_default<N_>(g, st);
-    PB_SMALL(1) PB_SMALL(2) PB_SMALL(3) PB_SMALL(5) PB_SMALL(6) PB_SMALL(7)
-    PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15)
+    PB_SMALL(9) PB_SMALL(10) PB_SMALL(11) PB_SMALL(12) PB_SMALL(13) PB_SMALL(14) PB_SMALL(15) PB_SMALL(16)
 #undef PB_SMALL
-    case 4:
-      return launch_small_tuned<4>(g, st);
-    case 8:
-      return launch_small_tuned<8>(g, st);
-    case 16:
-      return launch_small_tuned<16>(g, st);
     default:
       return cudaErrorInvalidValue;
   }

@@ -66,6 +66,12 @@ def _stream(dev):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
+def _on(dev):
+    """Run the native call with ``dev`` current: the library sizes grids and
+    caches launch attributes for the current device."""
+    return torch.cuda.device(dev)
+
+
 def _mark_diag(mat, dj, n, diagonal):
     # level3.py:69-74
     if diagonal:
@@ -109,8 +115,9 @@ def gemm_nt(m, n, k, alpha, A, B, beta, C, D):
     if m == 0 or n == 0 or nb == 0:
         return
     da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
-    _native.call("pb_dgemm_nt", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
-                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+    with _on(d.device):
+        _native.call("pb_dgemm_nt", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                     float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
 
 
 def gemm_nn(m, n, k, alpha, A, B, beta, C, D):
@@ -129,8 +136,9 @@ def gemm_nn(m, n, k, alpha, A, B, beta, C, D):
     if m == 0 or n == 0 or nb == 0:
         return
     da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
-    _native.call("pb_dgemm_nn", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
-                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+    with _on(d.device):
+        _native.call("pb_dgemm_nn", m, n, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                     float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
 
 
 def trmm_rlnn(m, n, alpha, A, B, D):
@@ -146,8 +154,12 @@ def trmm_rlnn(m, n, alpha, A, B, D):
     if m == 0 or n == 0 or nb == 0:
         return
     da, db, dd = (x.descriptor(nb) for x in (a, b, d))
-    _native.call("pb_dtrmm_rlnn", m, n, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
-                 ctypes.byref(dd), di, dj, _stream(d.device))
+    with _on(d.device):
+        need = _native.worksize("pb_dtrmm_rlnn", m, n, ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                                ctypes.byref(dd), di, dj)
+        ws, wp, wb = _native.workspace(need, d.device)
+        _native.call("pb_dtrmm_rlnn", m, n, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                     ctypes.byref(dd), di, dj, wp, wb, _stream(d.device))
 
 
 def syrk_ln(m, k, alpha, A, B, beta, C, D):
@@ -164,8 +176,9 @@ def syrk_ln(m, k, alpha, A, B, beta, C, D):
     if m == 0 or nb == 0:
         return
     da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
-    _native.call("pb_dsyrk_ln", m, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
-                 float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
+    with _on(d.device):
+        _native.call("pb_dsyrk_ln", m, k, float(alpha), ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                     float(beta), ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, _stream(d.device))
 
 
 # ---------------------------------------------------------------------------
@@ -204,9 +217,10 @@ def trsm_rltn(m, n, alpha, A, B, D, check=True):
     use_dA = 1 if (ai == aj and a.diag_inv_valid(aj, n)) else 0
     info = None if use_dA else torch.empty(nb, dtype=torch.int32, device=d.device)
     da, db, dd = (x.descriptor(nb) for x in (a, b, d))
-    _native.call("pb_dtrsm_rltn", m, n, float(alpha), ctypes.byref(da), ai, aj, use_dA, ctypes.byref(db), bi, bj,
-                 ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr() if info is not None else 0),
-                 _stream(d.device))
+    with _on(d.device):
+        _native.call("pb_dtrsm_rltn", m, n, float(alpha), ctypes.byref(da), ai, aj, use_dA, ctypes.byref(db), bi,
+                     bj, ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr() if info is not None else 0),
+                     _stream(d.device))
     if check and info is not None:
         f = _first_failure(info)
         if f is not None:
@@ -242,8 +256,11 @@ def potrf_l(m, C, D, n=None, check=True):
         return None
     info = torch.empty(nb, dtype=torch.int32, device=d.device)
     dc, dd = c.descriptor(nb), d.descriptor(nb)
-    _native.call("pb_dpotrf_l", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj,
-                 ctypes.c_void_p(info.data_ptr()), _stream(d.device))
+    with _on(d.device):
+        need = _native.worksize("pb_dpotrf_l", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj)
+        ws, wp, wb = _native.workspace(need, d.device)
+        _native.call("pb_dpotrf_l", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj,
+                     ctypes.c_void_p(info.data_ptr()), wp, wb, _stream(d.device))
     if check:
         f = _first_failure(info)
         if f is not None:
@@ -281,9 +298,13 @@ def syrk_potrf_ln(m, k, A, B, C, D, n=None, check=True):
         return None
     info = torch.empty(nb, dtype=torch.int32, device=d.device)
     da, db, dc, dd = (x.descriptor(nb) for x in (a, b, c, d))
-    _native.call("pb_dsyrk_potrf_ln", m, n, k, ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
-                 ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr()),
-                 _stream(d.device))
+    with _on(d.device):
+        need = _native.worksize("pb_dsyrk_potrf_ln", m, n, k, ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                                ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj)
+        ws, wp, wb = _native.workspace(need, d.device)
+        _native.call("pb_dsyrk_potrf_ln", m, n, k, ctypes.byref(da), ai, aj, ctypes.byref(db), bi, bj,
+                     ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, ctypes.c_void_p(info.data_ptr()),
+                     wp, wb, _stream(d.device))
     if check:
         f = _first_failure(info)
         if f is not None:
@@ -318,9 +339,10 @@ def _getrf(m, n, C, D, pivot, ipiv, check, name):
             raise DimensionError(f"ipiv needs shape ({nb}, >= {mn}) int64 on {d.device}, unit column stride")
     info = torch.empty(nb, dtype=torch.int32, device=d.device)
     dc, dd = c.descriptor(nb), d.descriptor(nb)
-    _native.call("pb_dgetrf", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, 1 if pivot else 0,
-                 ctypes.c_void_p(ipiv.data_ptr() if pivot else 0), ipiv.stride(0) if pivot else 0,
-                 ctypes.c_void_p(info.data_ptr()), _stream(d.device))
+    with _on(d.device):
+        _native.call("pb_dgetrf", m, n, ctypes.byref(dc), ci, cj, ctypes.byref(dd), di, dj, 1 if pivot else 0,
+                     ctypes.c_void_p(ipiv.data_ptr() if pivot else 0), ipiv.stride(0) if pivot else 0,
+                     ctypes.c_void_p(info.data_ptr()), _stream(d.device))
     if check:
         f = _first_failure(info)
         if f is not None:

@@ -99,6 +99,10 @@ def _check_window(mat, ai, aj, m, n, what):
             f"{mat.rows}x{mat.cols} matrix")
 
 
+def _dev_of(x):
+    return x.device
+
+
 def _stream(dev):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
@@ -121,8 +125,9 @@ def pack_matrix(src, m, n, dst):
         return
     dd = d.descriptor()
     base = s.data.data_ptr() + 8 * (si + sj * s.lda)
-    _native.call("pb_dpack_cm", m, n, ctypes.c_void_p(base), s.lda, s.data.stride(0), ctypes.byref(dd), di, dj,
-                 _stream(d.device))
+    with torch.cuda.device(_dev_of(d)):
+        _native.call("pb_dpack_cm", m, n, ctypes.c_void_p(base), s.lda, s.data.stride(0), ctypes.byref(dd), di, dj,
+                     _stream(d.device))
 
 
 def unpack_matrix(src, m, n, dst):
@@ -136,8 +141,9 @@ def unpack_matrix(src, m, n, dst):
         return
     ds = s.descriptor()
     base = d.data.data_ptr() + 8 * (di + dj * d.lda)
-    _native.call("pb_dunpack_cm", m, n, ctypes.byref(ds), si, sj, ctypes.c_void_p(base), d.lda, d.data.stride(0),
-                 _stream(s.device))
+    with torch.cuda.device(_dev_of(d)):
+        _native.call("pb_dunpack_cm", m, n, ctypes.byref(ds), si, sj, ctypes.c_void_p(base), d.lda, d.data.stride(0),
+                     _stream(s.device))
 
 
 def gecp(m, n, A, B):
@@ -151,7 +157,8 @@ def gecp(m, n, A, B):
     if m == 0 or n == 0 or d.batch == 0:
         return
     ds, dd = s.descriptor(d.batch), d.descriptor()
-    _native.call("pb_dgecp", m, n, ctypes.byref(ds), si, sj, ctypes.byref(dd), di, dj, _stream(d.device))
+    with torch.cuda.device(_dev_of(d)):
+        _native.call("pb_dgecp", m, n, ctypes.byref(ds), si, sj, ctypes.byref(dd), di, dj, _stream(d.device))
 
 
 def pack_array_into(t, dst, di=0, dj=0):
@@ -167,8 +174,9 @@ def pack_array_into(t, dst, di=0, dj=0):
     if t.dtype != torch.float64 or t.device != d.device:
         raise DimensionError("source must be a float64 tensor on the destination's device")
     dd = d.descriptor()
-    _native.call("pb_dpack", m, n, ctypes.c_void_p(t.data_ptr()), t.stride(1), t.stride(2), t.stride(0),
-                 ctypes.byref(dd), di, dj, _stream(d.device))
+    with torch.cuda.device(_dev_of(d)):
+        _native.call("pb_dpack", m, n, ctypes.c_void_p(t.data_ptr()), t.stride(1), t.stride(2), t.stride(0),
+                     ctypes.byref(dd), di, dj, _stream(d.device))
 
 
 def unpack_window(A, m, n, out=None):
@@ -180,8 +188,9 @@ def unpack_window(A, m, n, out=None):
     if m == 0 or n == 0 or a.batch == 0:
         return out
     da = a.descriptor()
-    _native.call("pb_dunpack", m, n, ctypes.byref(da), ai, aj, ctypes.c_void_p(out.data_ptr()), out.stride(1),
-                 out.stride(2), out.stride(0), _stream(a.device))
+    with torch.cuda.device(_dev_of(a)):
+        _native.call("pb_dunpack", m, n, ctypes.byref(da), ai, aj, ctypes.c_void_p(out.data_ptr()), out.stride(1),
+                     out.stride(2), out.stride(0), _stream(a.device))
     return out
 
 

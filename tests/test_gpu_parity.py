@@ -245,9 +245,10 @@ def spd_batch(rng, nb, n, shift=None):
 
 
 @pytest.mark.parametrize("mn", [(4, 4), (8, 8), (11, 11), (16, 16), (17, 17), (24, 24), (32, 32), (37, 37), (41, 41),
-                                (57, 57), (63, 63), (64, 64),
-                                (96, 96), (128, 128), (160, 160), (232, 232), (256, 256), (300, 300), (29, 13),
-                                (256, 128), (70, 33), (320, 240), (300, 264)])
+                                (57, 57), (63, 63), (64, 64), (65, 65), (72, 72), (90, 90), (96, 96), (113, 113),
+                                (120, 120), (128, 128), (129, 129), (136, 136), (160, 160), (200, 200), (232, 232),
+                                (256, 256), (300, 300), (29, 13), (256, 128), (70, 33), (320, 240), (300, 264),
+                                (520, 40), (600, 20), (600, 200), (520, 520)])
 def test_potrf_l_random_vs_oracle(mn):
     m, n = mn
     rng = np.random.default_rng(m * 7 + n)
@@ -271,10 +272,13 @@ def test_potrf_l_random_vs_oracle(mn):
         compare_storage(host(dD), D.storage, mask, m, f"potrf {mn} {oc}{od}")
 
 
-@pytest.mark.parametrize("n", [4, 8, 12, 16, 17, 24, 40, 57, 64, 128, 256, 300])
-def test_potrf_failure_index_and_partial_writes(n):
+@pytest.mark.parametrize("n", [4, 8, 12, 16, 17, 24, 40, 57, 64, 72, 100, 128, 136, 200, 256, 300])
+@pytest.mark.parametrize("off", [(0, 0), (1, 1)])
+def test_potrf_failure_index_and_partial_writes(n, off):
     """Bad pivots: info equals the reference's index, and the failing item is
-    written exactly as far as the reference writes it (ccore.pyx:884-899)."""
+    written exactly as far as the reference writes it (ccore.pyx:884-899);
+    an unaligned D window (di % 4 != 0) of a failing item is left untouched
+    except for diag_inv (level3.py:338-344)."""
     rng = np.random.default_rng(n)
     nb = 16
     a = spd_batch(rng, nb, n)
@@ -283,12 +287,12 @@ def test_potrf_failure_index_and_partial_writes(n):
         if b % 3 != 2:  # keep some items healthy
             a[b, fails[b], fails[b]] = -10.0 * n
     a[5, 0, 0] = np.nan  # NaN passes the d <= 0 test (ccore.pyx:423)
-    C = rand_batch(rng, nb, n, n)
-    C.set_window(0, 0, a)
-    D = rand_batch(rng, nb, n, n, fill=2.5)
+    C = rand_batch(rng, nb, n + off[0], n + off[1])
+    C.set_window(off[0], off[1], a)
+    D = rand_batch(rng, nb, n + off[0], n + off[1], fill=2.5)
     dC, dD = dev(C), dev(D)
-    info = level3.potrf_l(n, dC, dD, check=False).cpu().numpy()
-    winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
+    info = level3.potrf_l(n, dC.ref(*off), dD.ref(*off), check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C, off[0], off[1], D, off[0], off[1])
     assert np.array_equal(info, winfo)
     got = host(dD)
     for b in range(nb):
@@ -298,10 +302,63 @@ def test_potrf_failure_index_and_partial_writes(n):
         same = np.isclose(g, w, rtol=1e-11, atol=1e-11) | (gn & wn)
         assert np.all(same), (b, info[b])
     with pytest.raises(pb.NotPositiveDefiniteError) as ei:
-        level3.potrf_l(n, dC, dD)
+        level3.potrf_l(n, dC.ref(*off), dD.ref(*off))
     first = int(np.nonzero(winfo >= 0)[0][0])
     assert ei.value.batch_index == first and ei.value.index == winfo[first]
     assert not dD.diag_inv_valid(0, n)
+
+
+@pytest.mark.parametrize("n", [24, 40, 57, 64])
+def test_potrf_nonfinite_inputs_keep_reference_pattern(n):
+    """A NaN / Inf off the diagonal (17 <= n <= 64, the register-tile
+    kernel): the NaN/Inf pattern of D and info equal the reference's -- such
+    items are redone in the reference's own operation order (pb_exact.cu);
+    finite entries agree within tolerance."""
+    rng = np.random.default_rng(100 + n)
+    nb = 6
+    a = spd_batch(rng, nb, n)
+    i0 = n // 2 + 3
+    a[0, i0, 5] = np.nan           # row i0, early column
+    a[1, n - 1, n - 3] = np.nan     # last row
+    a[2, i0, i0 - 1] = np.inf       # next to the diagonal
+    a[3, 9, 2] = -np.inf
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    D = rand_batch(rng, nb, n, n, fill=0.5)
+    dC, dD = dev(C), dev(D)
+    info = level3.potrf_l(n, dC, dD, check=False).cpu().numpy()
+    winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
+    assert np.array_equal(info, winfo)
+    got = host(dD)
+    for b in range(nb):
+        g, w = got[b], D.storage[b]
+        assert np.array_equal(np.isnan(g), np.isnan(w)), (n, b)
+        assert np.array_equal(np.isinf(g), np.isinf(w)), (n, b)
+        fin = np.isfinite(w)
+        assert np.allclose(g[fin], w[fin], rtol=1e-11, atol=1e-11), (n, b)
+
+
+def test_potrf_concurrent_streams_disjoint_items():
+    """Two streams factor disjoint item ranges of one batch at the same time
+    (the stream contract in include/pb_b200.h): the result equals one call."""
+    rng = np.random.default_rng(77)
+    for n in (4, 8, 32, 100):
+        nb = 4096 if n <= 8 else 512
+        C = rand_batch(rng, nb, n, n)
+        C.set_window(0, 0, spd_batch(rng, nb, n))
+        dC = dev(C)
+        ref = alloc(nb, n, n, zero=True)
+        level3.potrf_l(n, dC, ref)
+        out = alloc(nb, n, n, zero=True)
+        half = nb // 2 + 1
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            level3.potrf_l(n, dC.shard(0, half), out.shard(0, half), check=False)
+        with torch.cuda.stream(s2):
+            level3.potrf_l(n, dC.shard(half, nb), out.shard(half, nb), check=False)
+        torch.cuda.synchronize()
+        assert torch.equal(out.item_storage(), ref.item_storage()), n
 
 
 @pytest.mark.parametrize("mn", [(2, 2), (5, 3), (8, 8), (3, 9), (13, 6), (72, 48), (40, 64), (33, 100), (16, 232),
@@ -1004,7 +1061,7 @@ def test_potrf_host_pinned_descriptors(n):
     info = torch.empty(nb, dtype=torch.int32, device="cuda")
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     assert _native.call("pb_dpotrf_l", n, n, ctypes.byref(dc), 0, 0, ctypes.byref(dd), 0, 0,
-                        ctypes.c_void_p(info.data_ptr()), st) == 0
+                        ctypes.c_void_p(info.data_ptr()), None, 0, st) == 0
     torch.cuda.synchronize()
     winfo = O.potrf_l(n, C, 0, 0, D, 0, 0)
     assert np.array_equal(info.cpu().numpy(), winfo)

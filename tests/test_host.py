@@ -179,17 +179,38 @@ def _header_symbols():
 def test_native_library_exports_header_surface():
     lib = _native.load()
     syms = _header_symbols()
-    assert len(syms) == 17, syms
+    assert len(syms) == 20, syms
     assert set(syms) == set(_native.SIGNATURES)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.pb_version() == 1
+    assert lib.pb_version() == _native.ABI_VERSION == 2
     # argument validation needs no device: a bad size returns -position
     d = pb.allocate_panel_batch(1, 4, 4, device="cpu").descriptor()
     assert lib.pb_dgemm_nt(-1, 4, 4, 1.0, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, 0.0, ctypes.byref(d), 0, 0,
                            ctypes.byref(d), 0, 0, None) == -1
     assert b"negative" in lib.pb_last_error()
-    assert lib.pb_dpotrf_l(4, 5, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, None, None) == -2
+    assert lib.pb_dpotrf_l(4, 5, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, None, None, 0, None) == -2
+    assert lib.pb_dpotrf_l_worksize(4, 5, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0) == -2
+    # workspace sizing (no device needed): direct kernels need none, blocked
+    # windows need panel workspace, unaligned blocked windows an aligned copy
+    big = pb.allocate_panel_batch(3, 300, 300, device="cpu").descriptor()
+    assert lib.pb_dpotrf_l_worksize(4, 4, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0) == 0
+    assert lib.pb_dpotrf_l_worksize(128, 128, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0) == 0
+    w256 = lib.pb_dpotrf_l_worksize(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0)
+    assert w256 >= 3 * 2 * 128 * 128 * 8  # W (128 x 128) + T (128 x 128) per item
+    assert lib.pb_dpotrf_l_worksize(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 1, 0) >= w256 + 3 * 256 * 256 * 8
+    assert lib.pb_dpotrf_l_worksize(600, 20, ctypes.byref(pb.allocate_panel_batch(2, 600, 20, device="cpu")
+                                                          .descriptor()), 0, 0,
+                                    ctypes.byref(pb.allocate_panel_batch(2, 600, 20, device="cpu").descriptor()),
+                                    0, 0) >= 2 * 580 * 20 * 8  # tall: rows below the square factor
+    # a call with less workspace than the query reports is refused before any launch
+    assert lib.pb_dpotrf_l(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0, ctypes.c_void_p(8), None, 0,
+                           None) == -10
+    assert b"workspace" in lib.pb_last_error()
+    assert lib.pb_dtrmm_rlnn_worksize(4, 40, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0, ctypes.byref(big), 0,
+                                      0) > 0  # in place, n > 24
+    assert lib.pb_dtrmm_rlnn_worksize(4, 8, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0, ctypes.byref(big), 0,
+                                      0) == 0
     assert lib.pb_dgemm_nt(4, 4, 4, 1.0, ctypes.byref(d), 1, 0, ctypes.byref(d), 0, 0, 0.0, ctypes.byref(d), 0, 0,
                            ctypes.byref(d), 0, 0, None) == -5
     assert lib.pb_dgetrf(4, 4, ctypes.byref(d), 0, 0, ctypes.byref(d), 0, 0, 1, None, 4, None, None) == -10
@@ -233,13 +254,13 @@ def test_bench_csv_matches_reference_schema(tmp_path):
     assert float(rows[0][5]) == (1.0 / 1e3) / 1000 and float(rows[-1][6]) == 70.0
     # extended sidecar: the same seven columns, then gpus, batch, GB/s, roofline
     for i, p in enumerate(points):
-        p.update(hbm_gbs_alg=100.0 * (i + 1), roofline_gflops=1000.0, roofline_frac=0.01 * (i + 1))
+        p.update(gbs_alg=100.0 * (i + 1), roofline_gflops=1000.0, roofline_frac=0.01 * (i + 1))
     ext = tmp_path / "sweep_ext.csv"
     bench.emit_csv_ext(bench.csv_rows(points, pts), points, pts, 2, str(ext))
     el = ext.read_text().splitlines()
     assert el[0].startswith(lines[0] + ",gpus,batch,")
     assert [e.split(",")[:7] for e in el[1:]] == rows
-    assert el[1].split(",")[7] == "2" and int(el[1].split(",")[8]) == 2 * pts[0].batch
+    assert el[1].split(",")[7] == "2" and int(el[1].split(",")[8]) == points[0]["items"]
 
 
 def test_fixture_formats_match_the_reference(tmp_path):
@@ -276,7 +297,7 @@ def test_fixture_formats_match_the_reference(tmp_path):
 def test_bench_flop_counts_follow_the_reference():
     """bench.Point.flops_item restates the reference's flop_count
     (pkg/src/panelblas/bench.py:85-105); KATs after its
-    tests/test_bench.py:13-21, plus bench.memsize == the matstore size."""
+    tests/test_bench.py:13-21, plus bench.split_bytes == the split-layout size."""
     import sys
     sys.path.insert(0, REPO)
     import bench
@@ -295,7 +316,7 @@ def test_bench_flop_counts_follow_the_reference():
         bench.Point("nope", 1, 1, 1, 1)
     for m in range(0, 41):
         for n in range(0, 41, 3):
-            assert bench.memsize(m, n) == memsize_panel_matrix(m, n)
+            assert bench.split_bytes(m, n) == sum(pb.memsize_split_batch(1, m, n))
     # every C2 point carries ~2^34 flops (BASELINE configs[1])
     pts, _ = bench.config_points("c2")
     assert [p.n for p in pts] == [4, 8, 16, 32, 64, 128, 256]
@@ -328,7 +349,8 @@ def test_bench_cli_reference_arm_and_exit_codes():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
-    r1 = _run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", env={"RANK": "1", "WORLD_SIZE": "2"})
+    r1 = _run_bench("--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+                    env={"RANK": "1", "WORLD_SIZE": "2"})
     assert r1.returncode == 0 and r1.stdout.strip() == ""
     rb = _run_bench("--config", "bogus")
     assert rb.returncode != 0 and "unknown config" in rb.stderr
