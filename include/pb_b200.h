@@ -125,11 +125,14 @@ int pb_dtrmm_rlnn(int m, int n, double alpha,
                   void *work, int64_t work_bytes, void *stream);
 
 /* D * A^T = alpha*B, A n x n lower non-unit, B and D m x n
- * (blasfeo_dtrsm_rltn).  Reciprocals of A's diagonal: use_dA != 0 reuses
+ * (blasfeo_dtrsm_rltn).  Reciprocals of A's diagonal: use_dA == 1 reuses
  * sA->dA[aj .. aj+n) written by a factorization (level3.py:169-170);
  * use_dA == 0 computes 1/A[j,j] in-kernel, and an item with a zero
- * diagonal gets info[b] = j and is left untouched (level3.py:171-177).
- * info may be NULL when use_dA != 0. */
+ * diagonal gets info[b] = j and is left untouched (level3.py:171-177);
+ * use_dA == 2 decides per item from info ON ENTRY (the factorization's
+ * per-item status): reuse where info[b] < 0, compute (with the zero-pivot
+ * rule) where the factorization failed and its diag_inv is therefore
+ * invalid (level3.py:346-349).  info may be NULL only when use_dA == 1. */
 int pb_dtrsm_rltn(int m, int n, double alpha,
                   const pb_dmat_batch *sA, int ai, int aj, int use_dA,
                   const pb_dmat_batch *sB, int bi, int bj,

@@ -321,11 +321,15 @@ int pb_dtrsm_rltn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
   if ((r = check_mat(sA, 4, ai, aj, n, n, batch, false))) return r;
   if ((r = check_mat(sB, 8, bi, bj, m, n, batch, false))) return r;
   if ((r = check_mat(sD, 11, di, dj, m, n, batch, true))) return r;
+  if (use_dA < 0 || use_dA > 2) return fail_arg(7, "use_dA must be 0, 1 or 2");
   if (use_dA && n > 0 && !sA->dA) return fail_arg(4, "use_dA set but the factor has no diag_inv");
-  if (!use_dA && !info) return fail_arg(14, "info is required when reciprocals are computed");
+  if (use_dA != 1 && !info) return fail_arg(14, "info is required when reciprocals may be computed");
   if (m == 0 || n == 0 || batch == 0) return 0;  // level3.py:200-201
   cudaStream_t st = (cudaStream_t)stream;
   if (trsm_fits(m, n)) return trsm_run(m, n, alpha, sA, ai, aj, use_dA, sB, bi, bj, sD, di, dj, info, nullptr, st);
+  // blocked windows decide once for the whole batch: use_dA == 2 computes
+  // every item's reciprocals (equal to the factorization's up to rounding)
+  if (use_dA == 2) use_dA = 0;
   // blocked path: the zero-pivot check covers the whole diagonal first, so a
   // singular item is left completely untouched (level3.py:171-177)
   if (info) {

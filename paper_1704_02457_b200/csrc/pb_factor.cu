@@ -477,8 +477,12 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
     cp_async_commit();
     cp_async_wait<0>();
     team_sync(bar, tthreads);
-    // reciprocals: reuse the factorization's, or compute (zero -> info)
-    if (g.use_dA) {
+    // reciprocals: reuse the factorization's, or compute (zero -> info);
+    // use_dA == 2 decides per item: reuse where the factorization succeeded
+    // (info on entry < 0), compute where it failed (its diag_inv is invalid,
+    // level3.py:346-349)
+    const bool reuse = g.use_dA == 1 || (g.use_dA == 2 && g.info[b] < 0);
+    if (reuse) {
       const double *dA = g.A.ditem(b);
       for (int c = ttid; c < n; c += tthreads) dinv[c] = dA[g.aj + c];
     } else {
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
     team_sync(bar, tthreads);
     // first zero pivot (level3.py:171-175): the item is then left untouched
     int fail = -1;
-    if (!g.use_dA) {
+    if (!reuse) {
       for (int c = 0; c < n; ++c)
         if (S[t.off(c, c)] == 0.0) { fail = c; break; }
     }

@@ -72,13 +72,15 @@ def _on(dev):
     return torch.cuda.device(dev)
 
 
-def _mark_diag(mat, dj, n, diagonal):
-    # level3.py:69-74
+def _mark_diag(mat, dj, n, diagonal, info=None):
+    # level3.py:69-74; `info`: per-item status of an unchecked factorization
+    # (failed items keep invalid reciprocals, level3.py:346-349)
     if diagonal:
         mat.diag_lo = dj
         mat.diag_hi = dj + n
     else:
         mat.diag_lo = mat.diag_hi = 0
+    mat.diag_info = info if (diagonal and n > 0) else None
 
 
 def _check_dinv(d, dj, w):
@@ -215,7 +217,15 @@ def trsm_rltn(m, n, alpha, A, B, D, check=True):
     if m == 0 or n == 0 or nb == 0:
         return None
     use_dA = 1 if (ai == aj and a.diag_inv_valid(aj, n)) else 0
-    info = None if use_dA else torch.empty(nb, dtype=torch.int32, device=d.device)
+    info = None
+    if use_dA and a.diag_info is not None:
+        # the factorization ran unchecked: reuse per item, recompute for the
+        # items it failed on (their diag_inv is invalid, level3.py:346-349)
+        use_dA = 2
+        src = a.diag_info if a.batch == nb else a.diag_info.expand(nb)
+        info = src.to(torch.int32).clone()
+    elif not use_dA:
+        info = torch.empty(nb, dtype=torch.int32, device=d.device)
     da, db, dd = (x.descriptor(nb) for x in (a, b, d))
     with _on(d.device):
         _native.call("pb_dtrsm_rltn", m, n, float(alpha), ctypes.byref(da), ai, aj, use_dA, ctypes.byref(db), bi,
@@ -268,7 +278,7 @@ def potrf_l(m, C, D, n=None, check=True):
             raise NotPositiveDefiniteError(
                 f"potrf_l: non-positive pivot at index {f[1]} (batch item {f[0]})", f[1],
                 batch_index=f[0], info=info)
-    _mark_diag(d, dj, n, di == dj)
+    _mark_diag(d, dj, n, di == dj, None if check else info)
     return info
 
 
@@ -312,7 +322,7 @@ def syrk_potrf_ln(m, k, A, B, C, D, n=None, check=True):
             raise NotPositiveDefiniteError(
                 f"syrk_potrf_ln: non-positive pivot at index {f[1]} (batch item {f[0]})", f[1],
                 batch_index=f[0], info=info)
-    _mark_diag(d, dj, n, di == dj)
+    _mark_diag(d, dj, n, di == dj, None if check else info)
     return info
 
 
@@ -349,7 +359,7 @@ def _getrf(m, n, C, D, pivot, ipiv, check, name):
             _mark_diag(d, dj, 0, False)
             raise SingularMatrixError(f"{name}: zero pivot at index {f[1]} (batch item {f[0]})", f[1],
                                       batch_index=f[0], info=info)
-    _mark_diag(d, dj, mn, di == dj)
+    _mark_diag(d, dj, mn, di == dj, None if check else info)
     return ipiv if pivot else info
 
 

@@ -109,7 +109,7 @@ class PanelBatch:
     """
 
     __slots__ = ("batch", "rows", "cols", "panel_size", "panel_length", "storage", "diag_storage",
-                 "memsize", "diag_lo", "diag_hi", "_diag_off", "_data_elems")
+                 "memsize", "diag_lo", "diag_hi", "diag_info", "_diag_off", "_data_elems")
 
     def __init__(self, batch, rows, cols, storage, diag_storage=None):
         self.batch = batch
@@ -124,6 +124,10 @@ class PanelBatch:
         self._diag_off = _round_up(self._data_elems * _ELEM, ALIGN) // _ELEM
         self.diag_lo = 0
         self.diag_hi = 0
+        # per-item status of that factorization when it ran unchecked
+        # (check=False): items with diag_info[b] >= 0 failed, so their
+        # reciprocals are not valid even inside [diag_lo, diag_hi)
+        self.diag_info = None
 
     def __repr__(self):
         return (f"PanelBatch({self.batch} x {self.rows}x{self.cols}, cn={self.panel_length}, "
@@ -179,7 +183,8 @@ class PanelBatch:
         return SubRef(self, ai, aj)
 
     def diag_inv_valid(self, ai, n):
-        """True if diag_inv covers columns [ai, ai+n) from a factorization."""
+        """True if diag_inv covers columns [ai, ai+n) from a factorization
+        (for every item whose ``diag_info`` does not say it failed)."""
         return self.diag_lo <= ai and ai + n <= self.diag_hi
 
     def _check_elem(self, b, ai, aj):
@@ -220,6 +225,7 @@ class PanelBatch:
         v = PanelBatch(hi - lo, self.rows, self.cols, self.storage[lo:hi],
                        None if self.diag_storage is None else self.diag_storage[lo:hi])
         v.diag_lo, v.diag_hi = self.diag_lo, self.diag_hi
+        v.diag_info = None if self.diag_info is None else self.diag_info[lo:hi]
         return v
 
     # ABI descriptor ---------------------------------------------------------

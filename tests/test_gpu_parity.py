@@ -338,6 +338,55 @@ def test_potrf_nonfinite_inputs_keep_reference_pattern(n):
         assert np.allclose(g[fin], w[fin], rtol=1e-11, atol=1e-11), (n, b)
 
 
+@pytest.mark.parametrize("mn", [(12, 8), (40, 24), (72, 48), (30, 64)])
+def test_trsm_reuse_after_unchecked_failing_potrf(mn):
+    """potrf_l(check=False) with failing items, then trsm_rltn on the factor:
+    healthy items reuse diag_inv, failed items recompute 1/A[j,j] like the
+    reference, whose failed potrf invalidates diag_inv (level3.py:346-349)."""
+    m, n = mn
+    rng = np.random.default_rng(m + 31 * n)
+    nb = 9
+    a = spd_batch(rng, nb, n)
+    bad = [1, 4, 7]
+    for b in bad:
+        f = int(rng.integers(1, n))
+        a[b, f, f] = -5.0 * n
+    a[4, 0, 0] = 0.0  # fails at pivot 0: its L is untouched, 1/A[0,0] of the old D -> zero pivot below
+    C = rand_batch(rng, nb, n, n)
+    C.set_window(0, 0, a)
+    L = rand_batch(rng, nb, n, n, fill=0.75)
+    dC, dL = dev(C), dev(L)
+    pinfo = level3.potrf_l(n, dC, dL, check=False)
+    winfo = O.potrf_l(n, C, 0, 0, L, 0, 0)
+    assert np.array_equal(pinfo.cpu().numpy(), winfo)
+    assert dL.diag_inv_valid(0, n) and dL.diag_info is not None
+    if 4 in bad:  # force a zero pivot on the failed item 4's stale diagonal
+        L.storage[4, O.element_offset(0, 0, L.cn)] = 0.0
+        dL = dev(L)
+        dL.diag_lo, dL.diag_hi, dL.diag_info = 0, n, pinfo
+    B = rand_batch(rng, nb, m, n)
+    X = rand_batch(rng, nb, m, n, fill=-2.0)
+    dB, dX = dev(B), dev(X)
+    info = level3.trsm_rltn(m, n, 1.0, dL, dB, dX, check=False).cpu().numpy()
+    got = host(dX)
+    ok = [b for b in range(nb) if b not in bad]
+    for idx, valid in ((ok, True), (bad, False)):
+        hL = O.HostBatch(len(idx), n, n, L.storage[idx].copy())
+        if valid:
+            hL.diag_lo, hL.diag_hi = 0, n
+        hB = O.HostBatch(len(idx), m, n, B.storage[idx].copy())
+        hX = O.HostBatch(len(idx), m, n, X.storage[idx].copy())
+        want_info = O.trsm_rltn(m, n, 1.0, hL, 0, 0, hB, 0, 0, hX, 0, 0)
+        assert np.array_equal(info[idx], want_info), (idx, info[idx], want_info)
+        mask = window_mask(hX, (0, 0), m, n)
+        for k, b in enumerate(idx):
+            compare_storage(got[b], hX.storage[k], mask, n, f"trsm reuse item {b}")
+    assert info[4] == 0
+    with pytest.raises(pb.SingularMatrixError) as ei:
+        level3.trsm_rltn(m, n, 1.0, dL, dB, dX)
+    assert ei.value.batch_index == 4
+
+
 def test_potrf_concurrent_streams_disjoint_items():
     """Two streams factor disjoint item ranges of one batch at the same time
     (the stream contract in include/pb_b200.h): the result equals one call."""

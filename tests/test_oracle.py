@@ -277,3 +277,99 @@ def test_oracle_riccati_composition_bit_exact_vs_reference_golden():
                 assert np.array_equal(F.storage[0, : want.size].view(np.uint64), want.view(np.uint64)), (r["name"], n)
             lnext, li = F, nu
         assert failed == r["status"], r["name"]
+
+
+@pytest.mark.skipif(ref_core is None, reason="oracle/_ref not built (make -C oracle ref)")
+@pytest.mark.parametrize("n", [64, 128, 256, 300])
+def test_oracle_matches_reference_core_at_baseline_sizes(n):
+    """The restatement against the reference's compiled core at the sizes the
+    BASELINE configs run (C1/C2/C3 up to n = 300), bit for bit: gemm_nt,
+    syrk_ln, potrf_l (+ diag_inv) and trsm_rltn reusing the fresh factor."""
+    rng = np.random.default_rng(1000 + n)
+    P = O.ctypes.c_void_p
+    sd = 4 * ((n + 3) // 4)
+    rows = sd
+    A = rng.standard_normal(rows * sd)
+    B = rng.standard_normal(rows * sd)
+    C = rng.standard_normal(rows * sd)
+    D1 = rng.standard_normal(rows * sd)
+    D2 = D1.copy()
+    ref_core.gemm_nt_drv(n, n, n, 1.0, A, 0, 0, sd, B, 0, 0, sd, 0.5, C, 0, 0, sd, D1, 0, 0, sd)
+    O.lib().po_gemm_nt(*[O._L(x) for x in (n, n, n)], O._D(1.0), A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                       B.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), O._D(0.5), C.ctypes.data_as(P), O._L(0),
+                       O._L(0), O._L(sd), D2.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd))
+    assert np.array_equal(D1.view(np.uint64), D2.view(np.uint64)), ("gemm", n)
+    S1 = rng.standard_normal(rows * sd)
+    S2 = S1.copy()
+    ref_core.syrk_ln_drv(n, n, -1.0, A, 0, 0, sd, A, 0, 0, sd, 1.0, C, 0, 0, sd, S1, 0, 0, sd)
+    O.lib().po_syrk_ln(O._L(n), O._L(n), O._D(-1.0), A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                       A.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), O._D(1.0), C.ctypes.data_as(P), O._L(0),
+                       O._L(0), O._L(sd), S2.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd))
+    assert np.array_equal(S1.view(np.uint64), S2.view(np.uint64)), ("syrk", n)
+    g = rng.uniform(-1, 1, (n, n))
+    spd = g @ g.T + n * np.eye(n)
+    Cs = np.zeros(rows * sd)
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    Cs[((ii - (ii & 3)) * sd + 4 * jj + (ii & 3)).ravel()] = spd.ravel()
+    L1 = np.full(rows * sd, 3.0)
+    L2 = L1.copy()
+    v1, v2 = np.zeros(n), np.zeros(n)
+    st1 = ref_core.potrf_drv(n, n, Cs, 0, 0, sd, L1, 0, 0, sd, v1, 0)
+    st2 = O.lib().po_potrf_l(O._L(n), O._L(n), Cs.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                             L2.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), v2.ctypes.data_as(P), O._L(0))
+    assert st1 == st2 == -1
+    assert np.array_equal(L1.view(np.uint64), L2.view(np.uint64)), ("potrf", n)
+    assert np.array_equal(v1.view(np.uint64), v2.view(np.uint64)), ("dinv", n)
+    X1 = np.zeros(rows * sd)
+    X2 = X1.copy()
+    ref_core.trsm_rltn_drv(n, n, 1.0, L1, 0, 0, sd, False, B, 0, 0, sd, X1, 0, 0, sd, v1, 0)
+    O.lib().po_trsm_rltn(O._L(n), O._L(n), O._D(1.0), L2.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd),
+                         O.ctypes.c_int(0), B.ctypes.data_as(P), O._L(0), O._L(0), O._L(sd), X2.ctypes.data_as(P),
+                         O._L(0), O._L(0), O._L(sd), v2.ctypes.data_as(P), O._L(0))
+    assert np.array_equal(X1.view(np.uint64), X2.view(np.uint64)), ("trsm", n)
+
+
+def test_oracle_pinned_to_reference_at_large_sizes():
+    """The oracle at C2/C3 sizes (potrf 128/256, gemm 128/300, trsm 128)
+    against digests of the REFERENCE's own outputs on the same seeded inputs
+    (tests/golden/make_golden_large.py): whole item storage, bit for bit."""
+    import hashlib
+    import json
+    import sys as _sys
+    _sys.path.insert(0, os.path.join(REPO, "tests", "golden"))
+    spec = json.load(open(os.path.join(REPO, "tests", "golden", "golden_large_v1.json")))
+
+    def inputs(case):  # same generator as make_golden_large.inputs (no reference import here)
+        rng = np.random.default_rng(case["seed"])
+        n = case["n"]
+        if case["op"] == "potrf_l":
+            g = rng.uniform(-1, 1, (n, n))
+            return {"C": g @ g.T + n * np.eye(n)}
+        if case["op"] == "gemm_nt":
+            return {"A": rng.standard_normal((n, n)), "B": rng.standard_normal((n, n))}
+        g = rng.uniform(-1, 1, (n, n))
+        return {"S": g @ g.T + n * np.eye(n), "B": rng.uniform(-1, 1, (n, n))}
+
+    def hb(arr):
+        h = O.HostBatch(1, *arr.shape)
+        h.set_window(0, 0, arr[None])
+        return h
+
+    for case in spec["cases"]:
+        n, a = case["n"], inputs(case)
+        if case["op"] == "potrf_l":
+            out = O.HostBatch(1, n, n)
+            assert O.potrf_l(n, hb(a["C"]), 0, 0, out, 0, 0)[0] == -1
+        elif case["op"] == "gemm_nt":
+            out = O.HostBatch(1, n, n)
+            O.gemm_nt(n, n, n, 1.0, hb(a["A"]), 0, 0, hb(a["B"]), 0, 0, 0.0, out, 0, 0, out, 0, 0)
+        else:
+            L = O.HostBatch(1, n, n)
+            O.potrf_l(n, hb(a["S"]), 0, 0, L, 0, 0)
+            out = O.HostBatch(1, n, n)
+            O.trsm_rltn(n, n, 1.0, L, 0, 0, hb(a["B"]), 0, 0, out, 0, 0)
+        raw = out.storage[0].view(np.uint8).tobytes()
+        assert len(raw) == case["bytes"], case["name"]
+        for p, v in case["samples"].items():
+            assert out.storage[0, int(p)] == float.fromhex(v), (case["name"], p)
+        assert hashlib.sha256(raw).hexdigest() == case["sha256"], case["name"]
