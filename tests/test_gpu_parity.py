@@ -1180,3 +1180,77 @@ def test_syrk_potrf_large_failure_partial_writes(m):
     mask = window_mask(D, (0, 0), m, m, lower=True)
     mask[D.diag_off: D.diag_off + m] = True
     compare_storage(host(dD), D.storage, mask, m, f"syrk_potrf {m} failure partial writes")
+
+
+# ---------------------------------------------------------------------------
+# guard bands (compute-sanitizer is closed on this GPU pool: own bounds checks)
+
+
+def _guarded(nb, m, n, fill=0.0, guard=1 << 17):
+    """A batch in the current layout carved from the middle of a larger
+    buffer whose guard regions (before and after every plane) hold a NaN
+    sentinel; returns (batch, check) where check() asserts the guards are
+    bit-for-bit untouched."""
+    sentinel = float.fromhex("-0x1.dead00beefp+1000")
+    planes = []
+    if LAYOUT == "interleaved":
+        per = pb.memsize_panel_matrix(m, n) // 8
+        buf = torch.full((2 * guard + nb * per,), sentinel, dtype=torch.float64, device="cuda")
+        core = buf[guard: guard + nb * per]
+        core.fill_(fill)
+        p = pb.create_panel_batch(nb, m, n, core)
+        planes.append((buf, guard, nb * per))
+    else:
+        de, dn = pb.panel_data_elems(m, n), min(m, n)
+        bd = torch.full((2 * guard + nb * de,), sentinel, dtype=torch.float64, device="cuda")
+        bg = torch.full((2 * guard + max(nb * dn, 1),), sentinel, dtype=torch.float64, device="cuda")
+        cd, cg = bd[guard: guard + nb * de], bg[guard: guard + nb * dn]
+        cd.fill_(fill)
+        cg.fill_(fill)
+        p = pb.create_panel_batch(nb, m, n, cd, cg)
+        planes += [(bd, guard, nb * de), (bg, guard, nb * dn)]
+
+    def check(what):
+        torch.cuda.synchronize()
+        for buf, g0, cnt in planes:
+            s = torch.tensor([sentinel], dtype=torch.float64, device="cuda").view(torch.int64)
+            head, tail = buf[:g0].view(torch.int64), buf[g0 + cnt:].view(torch.int64)
+            assert bool((head == s).all()) and bool((tail == s).all()), f"guard band written: {what}"
+    return p, check
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 40, 64, 100, 128, 256, 300])
+def test_guard_bands_potrf_and_trsm(n):
+    """Every potrf regime (and the trsm that follows) writes nothing outside
+    its operands' storage, including the blocked driver's workspace path."""
+    rng = np.random.default_rng(n)
+    nb = 3 if n >= 128 else 17
+    C, cchk = _guarded(nb, n, n)
+    pack.pack_array_into(torch.from_numpy(spd_batch(rng, nb, n)).cuda(), C)
+    D, dchk = _guarded(nb, n, n, fill=2.0)
+    level3.potrf_l(n, C, D, check=False)
+    level3.potrf_l(n, C, C, check=False)
+    X, xchk = _guarded(nb, 24, n)
+    level3.trsm_rltn(24, n, 1.0, D, X, X, check=False)
+    for ck, w in ((cchk, "C"), (dchk, "D"), (xchk, "X")):
+        ck(f"potrf/trsm n={n} {w}")
+
+
+@pytest.mark.parametrize("mnk", [(4, 4, 4), (20, 24, 9), (64, 64, 64), (100, 72, 40), (300, 264, 40)])
+def test_guard_bands_gemm_syrk_pack(mnk):
+    m, n, k = mnk
+    nb = max(2, 4000 // (m * n))
+    A, achk = _guarded(nb, m + 3, k)
+    B, bchk = _guarded(nb, n, k)
+    Cm, cchk = _guarded(nb, m, max(m, n))
+    D, dchk = _guarded(nb, m, max(m, n))
+    for x in (A, B, Cm):
+        x.storage.uniform_(-1, 1)
+    level3.gemm_nt(m, n, k, 1.0, A.ref(3, 0), B, 1.0, Cm, D)
+    level3.syrk_ln(m, k, -1.0, A, A, 1.0, Cm, D)
+    arr = torch.rand((nb, m, n), dtype=torch.float64, device="cuda")
+    pack.pack_array_into(arr, D)
+    pack.unpack_window(D, m, n)
+    pack.gecp(m, n, D, Cm)
+    for ck, w in ((achk, "A"), (bchk, "B"), (cchk, "C"), (dchk, "D")):
+        ck(f"gemm/syrk/pack {mnk} {w}")
