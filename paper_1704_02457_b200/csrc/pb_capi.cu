@@ -375,10 +375,13 @@ static size_t potrf_ws(int m, int n, int di, int batch) {
   if (potrf_direct(m, n)) return 0;
   if (di & 3) return panel_bytes(m, n) * batch + potrf_ws(m, n, 0, batch);
   const int n1 = m == n || n > 128 ? potrf_split(n) : n;
+  // step 1's own scratch (if its square is blocked too) is released before
+  // steps 2-4 take theirs (potrf_run resets the arena mark)
+  const size_t w1 = potrf_ws(n1, n1, 0, batch);
   size_t w = 0;
   if (m > n1) w += panel_bytes(m - n1, n1) * batch;
   if (n > n1) w += panel_bytes(m - n1, n - n1) * batch + potrf_ws(m - n1, n - n1, 0, batch);
-  return w;
+  return w1 > w ? w1 : w;
 }
 
 // rows of W (relative rows [0, rows)) item b may commit into D, see step 4
@@ -450,8 +453,10 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
     return potrf_commit(X, sD, di, dj, m, n, info, off, 0, 1, st);
   }
   const int n1 = m == n || n > 128 ? potrf_split(n) : n;
-  // 1. square factor of the first n1 columns
+  // 1. square factor of the first n1 columns (its scratch, if any, is free again afterwards)
+  const size_t mark = w.used;
   if ((r = potrf_run(n1, n1, sC, ci, cj, sD, di, dj, info, merge, off, w, st))) return r;
+  w.used = mark;
   if (m == n1) return 0;
   // 2. rows below against it, into workspace
   double *pw = w.take(panel_bytes(m - n1, n1) * batch);
