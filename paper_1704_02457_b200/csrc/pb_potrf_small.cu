@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(NTH, MINB) potrf_small1_kernel(PotrfArgs g) {
   const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
   const double *Cb = g.C.p;
   double *Db = g.D.p;
+  const bool inplace = g.C.p == g.D.p && g.C.stride == g.D.stride && g.C.cn == g.D.cn && g.ci == g.di && g.cj == g.dj;
 
   auto issue = [&](ix rd, int buf) {
     double *S = smem + buf * Cfg::BUF;
@@ -536,8 +537,10 @@ __global__ void __launch_bounds__(NTH, MINB) potrf_small1_kernel(PotrfArgs g) {
         }
       }
     const ix bi = b0 + it;
-    // D's bytes for the non-written part of every touched sector -> own slot
-    if (bi < g.batch) {
+    // D's bytes for the non-written part of every touched sector -> own slot;
+    // in place (D is C's window) the slot already holds them: C's staged
+    // prefix covers every touched sector, so the second round trip is skipped
+    if (bi < g.batch && !inplace) {
       const double *Di = Db + bi * g.D.stride;
 #pragma unroll
       for (int p = 0; p < NP; ++p)
@@ -671,7 +674,14 @@ cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
     case 1: return launch_small1<1>(g, st);
     case 2: return launch_small1<2>(g, st);
     case 3: return launch_small1<3>(g, st);
-    case 4: return launch_small1<4, 128, 1, 4>(g, st);
+    case 4: {
+      // in place the D-piece round trip is gone and the kernel is latency-bound:
+      // two stages at 3 CTAs/SM measured best (0.553 -> 0.625 of HBM; D != C
+      // stays single-stage, DRAM-saturated)
+      const bool ip = g.C.p == g.D.p && g.C.stride == g.D.stride && g.ci == g.di && g.cj == g.dj;
+      if (ip) return launch_small1<4, 128, 2, 3>(g, st);
+      return launch_small1<4, 128, 1, 4>(g, st);
+    }
     case 5: return launch_small1<5>(g, st);
     case 6: return launch_small1<6>(g, st);
     case 7: return launch_small1<7>(g, st);
