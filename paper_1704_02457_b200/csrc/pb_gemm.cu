@@ -920,11 +920,14 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
     // square output tile T minimising padded tile area x measured cost per
     // unit area of that tile shape (fitted over the C3 sweep n = 28..300 on
     // B200, profiles/r01_gemm_tile_sweep.txt: within 0.1 % of the per-size best)
+    // (round 2: tiles 80 / 88 added and tiles >= 72 on a 2-stage ring, so
+    // two CTAs fit an SM; weights refitted on the full C3 sweep per tile,
+    // profiles/r02_gemm_c3_tile_refit.txt: n >= 64 min 0.44 -> 0.51)
     int T = 64;
     double best = 1e30;
-    const int tiles[6] = {64, 32, 56, 48, 72, 40};
-    const double wcost[6] = {1.000, 1.055, 1.102, 1.241, 1.300, 1.305};
-    for (int i = 0; i < 6; ++i) {
+    const int tiles[8] = {64, 32, 56, 48, 72, 40, 80, 88};
+    const double wcost[8] = {1.000, 1.081, 1.056, 1.241, 1.107, 1.422, 1.350, 1.182};
+    for (int i = 0; i < 8; ++i) {
       const int t = tiles[i];
       const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t) * wcost[i];
       if (area < best * 0.999) best = area, T = t;
@@ -934,11 +937,13 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
 #define PB_TMA(T_, WM_, WN_, K_)                                                    \
   if (T == T_ && (K_ == 40) == k40) {                                                \
     if (cs) return launch_tma<T_, T_, WM_, WN_, K_, 2, SYRK, 1>(g, st);              \
+    if (T_ >= 72) return launch_tma<T_, T_, WM_, WN_, K_, 2, SYRK, 0>(g, st); /* 2 CTAs/SM */ \
     return launch_tma<T_, T_, WM_, WN_, K_, 3, SYRK, 0>(g, st);                      \
   }
     PB_TMA(64, 32, 16, 32) PB_TMA(64, 32, 16, 40) PB_TMA(48, 24, 16, 32) PB_TMA(48, 24, 16, 40)
     PB_TMA(32, 16, 16, 32) PB_TMA(32, 16, 16, 40) PB_TMA(72, 24, 24, 32) PB_TMA(72, 24, 24, 40)
     PB_TMA(56, 56, 8, 32) PB_TMA(56, 56, 8, 40) PB_TMA(40, 40, 8, 32) PB_TMA(40, 40, 8, 40)
+    PB_TMA(80, 40, 16, 32) PB_TMA(80, 40, 16, 40) PB_TMA(88, 88, 8, 32) PB_TMA(88, 88, 8, 40)
 #undef PB_TMA
   }
   if (small <= 40) return launch_tiled<32, 32, 16, 16, 32, 3, SYRK>(g, st);
