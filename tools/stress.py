@@ -35,33 +35,43 @@ def check(name, got, want, mask, n):
 
 
 def potrf_case(rng):
-    n = int(rng.integers(1, 81))
-    nb = int(rng.integers(1, 40))
+    # mostly the register/team sizes, sometimes the blocked driver (n > 128) and tall windows (m > n, any m)
+    n = int(rng.integers(1, 81)) if rng.random() < 0.7 else int(rng.integers(81, 301))
+    m = n if rng.random() < 0.7 else n + int(rng.integers(1, 4 if n > 200 else 400))
+    nb = int(rng.integers(1, 40 if n <= 80 else 5))
     oc = (int(rng.integers(0, 6)), int(rng.integers(0, 4)))
     od = (int(rng.integers(0, 3)) * 4 if rng.random() < 0.7 else int(rng.integers(0, 6)), int(rng.integers(0, 4)))
     g = rng.uniform(-1, 1, (nb, n, n))
-    a = g @ g.transpose(0, 2, 1) + n * np.eye(n)
+    a = np.zeros((nb, m, n))
+    a[:, :n] = g @ g.transpose(0, 2, 1) + n * np.eye(n)
+    a[:, n:] = rng.uniform(-1, 1, (nb, m - n, n))
     for b in range(nb):
         if rng.random() < 0.15:
             f = int(rng.integers(0, n))
             a[b, f, f] = -1.0
-    C = O.HostBatch(nb, oc[0] + n + 1, oc[1] + n + 2)
+    C = O.HostBatch(nb, oc[0] + m + 1, oc[1] + n + 2)
     C.storage[:] = rng.uniform(-1, 1, C.storage.shape)
     C.set_window(oc[0], oc[1], a)
-    D = O.HostBatch(nb, max(od[0], od[1]) + n + 2, od[1] + n + 1)  # diag_inv must hold dj + n
+    D = O.HostBatch(nb, max(od[0], od[1]) + m + 2, od[1] + n + 1)  # diag_inv must hold dj + n
     D.storage[:] = rng.uniform(-1, 1, D.storage.shape)
     dC, dD = dev(C), dev(D)
-    info = level3.potrf_l(n, dC.ref(*oc), dD.ref(*od), check=False).cpu().numpy()
-    winfo = O.potrf_l(n, C, *oc, D, *od)
-    assert np.array_equal(info, winfo), ("potrf info", n, oc, od)
+    info = level3.potrf_l(m, dC.ref(*oc), dD.ref(*od), n=n, check=False).cpu().numpy()
+    winfo = O.potrf_l(m, C, *oc, D, *od, n=n)
+    assert np.array_equal(info, winfo), ("potrf info", m, n, oc, od)
     mask = np.zeros(D.storage.shape[1], dtype=bool)
     for j in range(n):
-        for i in range(j, n):
+        for i in range(j, m):
             mask[O.element_offset(od[0] + i, od[1] + j, D.cn)] = True
     mask[D.diag_off + od[1]: D.diag_off + od[1] + n] = True
     ok = winfo < 0
+    got = host(dD)
     if ok.any():
-        check(f"potrf n={n} {oc}{od}", host(dD)[ok], D.storage[ok], mask, n)
+        check(f"potrf {m}x{n} {oc}{od}", got[ok], D.storage[ok], mask, m)
+    # failing items: exactly the reference's partial write set (elementwise, FP tolerance)
+    for b in np.nonzero(~ok)[0]:
+        gb, wb = got[b, : D.storage.shape[1]], D.storage[b]
+        same = np.isclose(gb, wb, rtol=1e-10, atol=1e-10) | (np.isnan(gb) & np.isnan(wb))
+        assert same.all(), ("potrf failing item", m, n, oc, od, int(winfo[b]))
 
 
 def getrf_case(rng):
