@@ -784,9 +784,9 @@ def run_e2e(args, gps, device, world, rank):
     level3.potrf_l, and reads the results device->host (D's data plane and
     diag_inv plane); four streams with their own device staging buffers
     keep both copy directions busy (a stream's next upload waits only for
-    its own previous download).  A bounded
-    pinned host buffer holds one sub-chunk of inputs; it is re-sent for
-    every sub-chunk (the data are synthetic either way)."""
+    its own previous download).  A bounded pinned host buffer per point
+    holds one sub-chunk of inputs; it is re-sent for every sub-chunk (the
+    data are synthetic either way)."""
     import torch
     import paper_1704_02457_b200 as pb
     from paper_1704_02457_b200 import level3
@@ -798,35 +798,48 @@ def run_e2e(args, gps, device, world, rank):
         if pt.op != "potrf_l":
             return None
         n = pt.n
-        per = split_bytes(n, n)
-        sub = max(1, min(gp.nb, int(128e6 // per)))
-        C = gp.ops["C"]
-        host_in = C.storage[:sub].cpu().pin_memory()
-        host_out = [(torch.empty_like(C.storage[:sub], device="cpu").pin_memory(),
-                     torch.empty((sub, n), dtype=torch.float64).pin_memory()) for _ in streams]
-        stage = [(pb.allocate_panel_batch(sub, n, n, device=device), pb.allocate_panel_batch(sub, n, n, device=device))
-                 for _ in streams]
-        plans.append((gp, sub, host_in, host_out, stage))
+        sub = max(1, min(gp.nb, int(128e6 // split_bytes(n, n))))
+        host_in = gp.ops["C"].storage[:sub].cpu().pin_memory()  # this point's inputs (per point)
+        plans.append((gp, sub, host_in))
+    # per-stream result / staging buffers shared by all points (host pinned
+    # memory stays ~1.5 GB per rank however many points)
+    out_elems = max(sub * (pb.panel_data_elems(gp.pt.n, gp.pt.n) + gp.pt.n) for gp, sub, _ in plans)
+    host_raw = [torch.empty(out_elems, dtype=torch.float64).pin_memory() for _ in streams]
+    dev_raw = [(torch.empty(out_elems, dtype=torch.float64, device=device),
+                torch.empty(out_elems, dtype=torch.float64, device=device)) for _ in streams]
+
+    vcache = {}
+
+    def views(k, n, cnt):
+        key = (k, n, cnt)
+        if key in vcache:
+            return vcache[key]
+        de = pb.panel_data_elems(n, n)
+        hr = host_raw[k]
+        hd, hg = hr[: cnt * de].view(cnt, de), hr[cnt * de: cnt * de + cnt * n].view(cnt, n)
+        ci, co = dev_raw[k]
+        cin = pb.create_panel_batch(cnt, n, n, ci[: cnt * de], ci[cnt * de: cnt * de + cnt * n])
+        dout = pb.create_panel_batch(cnt, n, n, co[: cnt * de], co[cnt * de: cnt * de + cnt * n])
+        vcache[key] = (hd, hg, cin, dout)
+        return vcache[key]
+
     h2d = d2h = 0
 
     def one_step(count=False):
         nonlocal h2d, d2h
         k = 0
-        for gp, sub, host_in, host_out, stage in plans:
+        for gp, sub, host_in in plans:
             n_items = items_of(gp.plan)
             for s0 in range(0, n_items, sub):
                 cnt = min(sub, n_items - s0)
                 st = streams[k % len(streams)]
-                hd, hg = host_out[k % len(streams)]
-                cin, dout = stage[k % len(streams)]
+                hd, hg, cin, dout = views(k % len(streams), gp.pt.n, cnt)
                 k += 1
                 with torch.cuda.stream(st):
-                    if cnt < sub:
-                        cin, dout = cin.shard(0, cnt), dout.shard(0, cnt)
                     cin.storage.copy_(host_in[:cnt], non_blocking=True)
                     level3.potrf_l(gp.pt.n, cin, dout, check=False)
-                    hd[:cnt].copy_(dout.storage, non_blocking=True)
-                    hg[:cnt].copy_(dout.diag_storage, non_blocking=True)
+                    hd.copy_(dout.storage, non_blocking=True)
+                    hg.copy_(dout.diag_storage, non_blocking=True)
                 if count:
                     h2d += cin.storage.numel() * 8
                     d2h += (dout.storage.numel() + dout.diag_storage.numel()) * 8
