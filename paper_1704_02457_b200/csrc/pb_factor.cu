@@ -56,39 +56,6 @@ __device__ __forceinline__ void tri_load(double *S, const Tri &t, const double *
   }
 }
 
-// Bulk-copy variant of tri_load for panel-aligned, 16-byte aligned items:
-// every (row group, half) of the tri layout is ONE contiguous run of the
-// item's panel (4 rows x min(width, n) columns), so thread 0 issues one
-// cp.async.bulk per run (completion on the team's mbarrier) and the other
-// threads only zero the padding columns [n, width) and the rows past m.
-// Rows of a partial last panel are read as stored (they only ever feed
-// their own rows and are never written back).
-__device__ __forceinline__ void tri_load_bulk(double *S, const Tri &t, const double *C, ix cn, ix ci, ix cj, int m,
-                                              int n, int gm, uint64_t *tbar, int ttid, int tthreads) {
-  if (ttid == 0) {
-    unsigned bytes = 0;
-    for (int gg = 0; gg < gm; ++gg)
-      for (int h = 0; h < 2; ++h)
-        if (8 * gg + 4 * h < m) bytes += 32u * (unsigned)min(t.width(gg), n);
-    mbar_arrive_expect_tx(tbar, bytes);
-    for (int gg = 0; gg < gm; ++gg) {
-      const int w = t.width(gg), base = t.group_off(gg);
-      for (int h = 0; h < 2; ++h) {
-        const int r0 = 8 * gg + 4 * h;
-        if (r0 < m) tma_load_1d(S + base + h * 4 * w, C + eo(ci + r0, cj, cn), 32u * (unsigned)min(w, n), tbar);
-      }
-    }
-  }
-  for (int gg = 0; gg < gm; ++gg) {
-    const int w = t.width(gg), base = t.group_off(gg);
-    for (int h = 0; h < 2; ++h) {
-      const int r0 = 8 * gg + 4 * h;
-      const int c0 = r0 < m ? min(w, n) : 0;
-      for (int q = ttid; q < 4 * (w - c0); q += tthreads) S[base + h * 4 * w + 4 * c0 + q] = 0.0;
-    }
-  }
-}
-
 // Stage a rows x k window (rows padded to rpad with zeros, columns to kp)
 // into a plain panel-major buffer of panel length kp.
 __device__ __forceinline__ void panel_load(double *S, int kp, const double *X, ix cn, ix xi, ix xj, int rows, int rpad,
@@ -589,6 +556,7 @@ bool potrf_fits(ix m, ix n) {
 cudaError_t run_potrf_l(const PotrfArgs &g, cudaStream_t st) {
   if (potrf_small_ok(g)) return run_potrf_small(g, st);
   if (potrf_reg_ok(g)) return run_potrf_reg(g, st);
+  if (potrf_chain_ok(g)) return run_potrf_chain(g, st);
   const ix gm = (g.m + 7) / 8;
   const bool db = Tri::size(g.m, g.n) * 8 <= 40 * 1024;  // double-buffer while it fits 2+ teams/SM
   const ix gn = (g.n + 7) / 8;

@@ -108,6 +108,8 @@ bool potrf_small_ok(const PotrfArgs &g);
 bool potrf_reg_ok(const PotrfArgs &g);
 cudaError_t run_potrf_reg(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st);
+bool potrf_chain_ok(const PotrfArgs &g);
+cudaError_t run_potrf_chain(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_exact_fixup(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
 size_t getrf_smem(int m, int n);

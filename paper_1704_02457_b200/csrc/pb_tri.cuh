@@ -179,4 +179,38 @@ __device__ __forceinline__ void apply_inv_block(double (&acc)[2], const double *
 }
 
 
+// Bulk-copy staging of an item into the tri layout for panel-aligned, 16-byte aligned items:
+// every (row group, half) of the tri layout is ONE contiguous run of the
+// item's panel (4 rows x min(width, n) columns), so thread 0 issues one
+// cp.async.bulk per run (completion on the team's mbarrier) and the other
+// threads only zero the padding columns [n, width) and the rows past m.
+// Rows of a partial last panel are read as stored (they only ever feed
+// their own rows and are never written back).
+__device__ __forceinline__ void tri_load_bulk(double *S, const Tri &t, const double *C, ix cn, ix ci, ix cj, int m,
+                                              int n, int gm, uint64_t *tbar, int ttid, int tthreads) {
+  if (ttid == 0) {
+    unsigned bytes = 0;
+    for (int gg = 0; gg < gm; ++gg)
+      for (int h = 0; h < 2; ++h)
+        if (8 * gg + 4 * h < m) bytes += 32u * (unsigned)min(t.width(gg), n);
+    mbar_arrive_expect_tx(tbar, bytes);
+    for (int gg = 0; gg < gm; ++gg) {
+      const int w = t.width(gg), base = t.group_off(gg);
+      for (int h = 0; h < 2; ++h) {
+        const int r0 = 8 * gg + 4 * h;
+        if (r0 < m) tma_load_1d(S + base + h * 4 * w, C + eo(ci + r0, cj, cn), 32u * (unsigned)min(w, n), tbar);
+      }
+    }
+  }
+  for (int gg = 0; gg < gm; ++gg) {
+    const int w = t.width(gg), base = t.group_off(gg);
+    for (int h = 0; h < 2; ++h) {
+      const int r0 = 8 * gg + 4 * h;
+      const int c0 = r0 < m ? min(w, n) : 0;
+      for (int q = ttid; q < 4 * (w - c0); q += tthreads) S[base + h * 4 * w + 4 * c0 + q] = 0.0;
+    }
+  }
+}
+
+
 }  // namespace pb
