@@ -43,34 +43,33 @@ __device__ __forceinline__ double dneg(double x) {
   return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
 }
 
-// NX[i] = -C(g_i, c) + sum_{k-steps < nk} L(g_i, .) L(c, .)^T for the active slots
-template <bool A0, bool A1>
-__device__ __forceinline__ void lookahead_slots(double (&NX)[2][2], const double *S, int fb, int fa0, int fa1, int ao0,
-                                                int ao1, int c, int nk) {
-  if (A0) {
-    NX[0][0] = dneg(S[ao0 + 32 * c]);
-    NX[0][1] = dneg(S[ao0 + 32 * c + 4]);
-  }
-  if (A1) {
-    NX[1][0] = dneg(S[ao1 + 32 * c]);
-    NX[1][1] = dneg(S[ao1 + 32 * c + 4]);
+// NX[s] = -C(g_s, c) + sum_{k-steps < nk} L(g_s, .) L(c, .)^T for slots F..NS-1
+template <int F, int NS>
+__device__ __forceinline__ void lookahead_slots(double (&NX)[3][2], const double *S, int fb, const int (&fa)[3],
+                                                const int (&ao)[3], int c, int nk) {
+#pragma unroll
+  for (int s = F; s < NS; ++s) {
+    NX[s][0] = dneg(S[ao[s] + 32 * c]);
+    NX[s][1] = dneg(S[ao[s] + 32 * c + 4]);
   }
 #pragma unroll 4
   for (int kk = 0; kk < nk; ++kk) {
     const double bv = S[fb + 16 * kk];
-    if (A0) dmma(NX[0], S[fa0 + 16 * kk], bv);
-    if (A1) dmma(NX[1], S[fa1 + 16 * kk], bv);
+#pragma unroll
+    for (int s = F; s < NS; ++s) dmma(NX[s], S[fa[s] + 16 * kk], bv);
   }
 }
 
 constexpr int CHAIN_THREADS = 256;
+constexpr int STEP_THREADS = 7 * 32;  // chain warp + six bulk warps meet at the step barriers
 
-// producer / consumer halves of a named barrier joined by the whole CTA
-__device__ __forceinline__ void bar_sync_all(int id) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(CHAIN_THREADS) : "memory");
+template <int N>
+__device__ __forceinline__ void bar_sync_n(int id) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(N) : "memory");
 }
-__device__ __forceinline__ void bar_arrive_all(int id) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(CHAIN_THREADS) : "memory");
+template <int N>
+__device__ __forceinline__ void bar_arrive_n(int id) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(N) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
@@ -88,17 +87,49 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
   double *S = smem;
   double *dinv = S + 32 * gn * (gn + 1);                    // cn8 reciprocals
   double *Wp = dinv + t.cn8;                                // 2 x 64: inverted diagonal block, lane-linear
-  double *Xp = Wp + 128;                                    // 2 x 64: solved tile of row j+1, lane-linear
-  uint64_t *tbar = reinterpret_cast<uint64_t *>(Xp + 128);  // bulk-load barrier
-  volatile int *flagv = reinterpret_cast<volatile int *>(tbar + 1);  // failing column per step (16)
+  double *Xp = Wp + 128;                                    // 2 x 64: solved tile (j+1, j), lane-linear
+  double *Mb = Xp + 128;                                    // 2 x 128: hand-off of row j+1's two chain tiles
+  uint64_t *tbar = reinterpret_cast<uint64_t *>(Mb + 256);  // bulk-load barrier
+  volatile int *flagv = reinterpret_cast<volatile int *>(tbar + 1);  // failing column per step (16) + item (1)
 
-  // per-warp constants: rows tw and tw + 8 (slot 0 / 1)
-  const int g0 = tw, g1 = tw + 8;
-  const bool has1 = g1 < gn;
-  const int g1c = has1 ? g1 : gn - 1;
-  const int fa0 = tri_frag(t, g0, 0, lane), fa1 = tri_frag(t, g1c, 0, lane);
-  const int ao0 = t.group_off(g0) + (r >> 2) * 4 * t.width(g0) + 8 * q + (r & 3);
-  const int ao1 = t.group_off(g1c) + (r >> 2) * 4 * t.width(g1c) + 8 * q + (r & 3);
+  // Roles by hardware scheduler.  The chain's ~20 dependent FP64 instructions
+  // per column queue behind every DMMA issued on the same sub-partition (one
+  // m8n8k4 holds its FP64 pipe for 16 cycles), so the chain warps of all CTAs
+  // on an SM are put on sub-partition 0 and no bulk work runs there.  The
+  // hardware rotates a CTA's warps over the sub-partitions per resident CTA
+  // (tools/warp_slots.cu: slots 0-7, 9 10 11 8 13 ..., 18 19 16 17 ...), so the
+  // roles come from %warpid, not from the warp index: the two warps whose
+  // slot % 4 == 0 are the chain warp and an idle stager, the other six own
+  // the row groups cyclically (bw, bw + 6, bw + 12).  (Performance only: any
+  // assignment is correct.)
+  int *role = reinterpret_cast<int *>(tbar + 1) + 20;
+  {
+    unsigned slot;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(slot));
+    if (lane == 0) role[tw] = (int)(slot & 3);
+  }
+  __syncthreads();
+  int chain_w = -1, stage_w = -1;
+#pragma unroll
+  for (int w = 0; w < 8; ++w)
+    if (role[w] == 0) {
+      if (chain_w < 0) chain_w = w;
+      else if (stage_w < 0) stage_w = w;
+    }
+  if (chain_w < 0) chain_w = 0;
+  if (stage_w < 0) stage_w = (chain_w + 4) & 7;
+  const bool is_chain = tw == chain_w, is_bulk = tw != chain_w && tw != stage_w;
+  const int bw = tw - (tw > chain_w) - (tw > stage_w);
+  const int ro = (r >> 2) * 4, lo = 8 * q + (r & 3);  // accumulator-layout offsets inside a tile row
+  int fa[3], ao[3], gs[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    gs[s] = bw + 6 * s;
+    const int gc = min(max(gs[s], 0), gn - 1);
+    fa[s] = tri_frag(t, gc, 0, lane);
+    ao[s] = t.group_off(gc) + ro * t.width(gc) + lo;
+  }
+  const int ns = !is_bulk ? 0 : (gs[2] < gn ? 3 : (gs[1] < gn ? 2 : 1));
 
   if (tid == 0) {
     mbar_init(tbar, 1);
@@ -138,121 +169,126 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
     while (nb < g.batch && skip(nb)) nb += stride;
     mbar_wait(tbar, tphase);
     tphase ^= 1;
-    if (tid < 16) flagv[tid] = -1;
+    if (tid < 17) flagv[tid] = -1;
     __syncthreads();
-    // next item's lower panel prefixes into L2 while this one is factored
-    if (tw == 7 && nb < g.batch && 4 * lane < n)
-      prefetch_l2(g.C.item(nb) + eo(g.ci + 4 * lane, g.cj, g.C.cn), 32u * (unsigned)min(4 * lane + 4, n));
-
-    // P: this warp's tiles of the current column block, fully downdated;
-    // NX: negated partial sums of the next column block (look-ahead)
-    double P[2][2], NX[2][2];
-    P[0][0] = S[ao0], P[0][1] = S[ao0 + 4];
-    P[1][0] = S[ao1], P[1][1] = S[ao1 + 4];
-    NX[0][0] = dneg(S[ao0 + 32]), NX[0][1] = dneg(S[ao0 + 36]);
-    NX[1][0] = dneg(S[ao1 + 32]), NX[1][1] = dneg(S[ao1 + 36]);
-    int fail = -1;
-    for (int jb = 0; jb < gn; ++jb) {
-      const unsigned par = (step + jb) & 1;
-      const int d = jb & 7, nd = (jb + 1) & 7;
-      const int ncol = min(8, n - 8 * jb);
-      const int wofs = (jb & 1) * 64 + lane;
-      double wb0, wb1;
-      if (tw == d) {
-        // ---- diagonal warp: factor + invert the 8x8 tile, publish W
-        const bool ds = jb >= 8;
-        double dg[2], wi[2];
-        dg[0] = ds ? P[1][0] : P[0][0];
-        dg[1] = ds ? P[1][1] : P[0][1];
-        const int f = factor_inv_tile(dg, wi, ncol, dinv + 8 * jb, lane);
-        const int aod = (ds ? ao1 : ao0) + 32 * jb;
+    if (is_chain) {
+      // ---- the pivot chain: factor(jb) -> solve tile (jb+1, jb) -> diag(jb+1)
+      double dg[2];
+      dg[0] = S[ro * 8 + lo], dg[1] = S[ro * 8 + lo + 4];
+      for (int jb = 0; jb < gn; ++jb) {
+        const int par = (step + jb) & 1;
+        const int ncol = min(8, n - 8 * jb);
+        const int wofs = (jb & 1) * 64 + lane;
+        double wi[2];
+        const int f = factor_inv_tile_u(dg, wi, ncol, dinv + 8 * jb, lane);
+        const int aod = t.group_off(jb) + ro * t.width(jb) + lo + 32 * jb;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * q + e;
           if (c < ncol && (f < 0 || c < f)) S[aod + 4 * e] = dg[e];
         }
-        if (f >= 0 && lane == 0) flagv[jb] = 8 * jb + f;
+        if (f >= 0 && lane == 0) flagv[jb] = flagv[16] = 8 * jb + f;
         Wp[wofs] = wi[0];
         Wp[wofs + 32] = wi[1];
-        wb0 = wi[0], wb1 = wi[1];
         __syncwarp();
-        bar_arrive_all(1 + par);
-      } else {
-        bar_sync_all(1 + par);
-        wb0 = Wp[wofs];
-        wb1 = Wp[wofs + 32];
-      }
-      fail = flagv[jb];
-      const bool s0 = g0 > jb, s1 = has1 && g1 > jb;  // slots with a tile below the diagonal
-      double X[2][2];
-      if (fail < 0) {
-        // ---- solve: X = P * W^T (the accumulator IS the A operand)
-        if (s0) {
-          X[0][0] = X[0][1] = 0.0;
-          dmma(X[0], P[0][0], wb0);
-          dmma(X[0], P[0][1], wb1);
-          S[ao0 + 32 * jb] = X[0][0];
-          S[ao0 + 32 * jb + 4] = X[0][1];
+        bar_arrive_n<STEP_THREADS>(1 + par);
+        const bool last = jb + 1 == gn;
+        double ps[2], nx[2];
+        if (!last) {
+          // row jb+1's tiles (jb+1, jb) and -(jb+1, jb+1), downdated over blocks < jb by their owner
+          bar_sync_n<64>(5 + par);
+          const int mo = (jb & 1) * 128 + lane;
+          ps[0] = Mb[mo], ps[1] = Mb[mo + 32];
+          nx[0] = Mb[mo + 64], nx[1] = Mb[mo + 96];
         }
-        if (s1) {
-          X[1][0] = X[1][1] = 0.0;
-          dmma(X[1], P[1][0], wb0);
-          dmma(X[1], P[1][1], wb1);
-          S[ao1 + 32 * jb] = X[1][0];
-          S[ao1 + 32 * jb + 4] = X[1][1];
+        if (f >= 0 || last) break;
+        double X[2] = {0.0, 0.0};
+        dmma(X, ps[0], wi[0]);
+        dmma(X, ps[1], wi[1]);
+        const int aox = t.group_off(jb + 1) + ro * t.width(jb + 1) + lo + 32 * jb;
+        S[aox] = X[0];
+        S[aox + 4] = X[1];
+        Xp[wofs] = X[0];
+        Xp[wofs + 32] = X[1];
+        __syncwarp();
+        bar_arrive_n<STEP_THREADS>(3 + par);
+        dmma(nx, X[0], X[0]);
+        dmma(nx, X[1], X[1]);
+        dg[0] = dneg(nx[0]), dg[1] = dneg(nx[1]);
+      }
+    } else if (is_bulk) {
+      // next item's lower panel prefixes into L2 while this one is factored
+      if (bw == 5 && nb < g.batch && 4 * lane < n)
+        prefetch_l2(g.C.item(nb) + eo(g.ci + 4 * lane, g.cj, g.C.cn), 32u * (unsigned)min(4 * lane + 4, n));
+      // P: this warp's tiles of the current column block, fully downdated;
+      // NX: negated partial sums of the next column block (look-ahead)
+      double P[3][2], NX[3][2], X[3][2];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        P[s][0] = S[ao[s]], P[s][1] = S[ao[s] + 4];
+        NX[s][0] = dneg(S[ao[s] + 32]), NX[s][1] = dneg(S[ao[s] + 36]);
+      }
+      if (bw == 1 && gn > 1) {  // hand row 1's tiles to the chain
+        Mb[lane] = P[0][0], Mb[lane + 32] = P[0][1];
+        Mb[lane + 64] = NX[0][0], Mb[lane + 96] = NX[0][1];
+        __syncwarp();
+        bar_arrive_n<64>(5 + (step & 1));
+      }
+      for (int jb = 0; jb < gn; ++jb) {
+        const int par = (step + jb) & 1;
+        const int wofs = (jb & 1) * 64 + lane;
+        bar_sync_n<STEP_THREADS>(1 + par);
+        if (flagv[jb] >= 0 || jb + 1 == gn) break;
+        const double wb0 = Wp[wofs], wb1 = Wp[wofs + 32];
+        // ---- solve X = P * W^T for rows >= jb + 2 (the accumulator IS the A operand)
+        const int c = jb + 2;
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+          if (s < ns && gs[s] >= c) {
+            X[s][0] = X[s][1] = 0.0;
+            dmma(X[s], P[s][0], wb0);
+            dmma(X[s], P[s][1], wb1);
+            S[ao[s] + 32 * jb] = X[s][0];
+            S[ao[s] + 32 * jb + 4] = X[s][1];
+          }
+        bar_sync_n<STEP_THREADS>(3 + par);
+        if (c >= gn) continue;  // nothing below row jb + 1
+        // ---- column block jb + 1: P = -(NX + X * L(jb+1, jb)^T)
+        const double xb0 = Xp[wofs], xb1 = Xp[wofs + 32];
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+          if (s < ns && gs[s] >= c) {
+            dmma(NX[s], X[s][0], xb0);
+            dmma(NX[s], X[s][1], xb1);
+            P[s][0] = dneg(NX[s][0]), P[s][1] = dneg(NX[s][1]);
+          }
+        // ---- look-ahead: column block jb + 2 over the solved blocks 0..jb
+        const int fb = tri_frag(t, c, 0, lane), nk = 2 * (c - 1);
+        if (ns == 3) {
+          if (gs[0] >= c) lookahead_slots<0, 3>(NX, S, fb, fa, ao, c, nk);
+          else if (gs[1] >= c) lookahead_slots<1, 3>(NX, S, fb, fa, ao, c, nk);
+          else if (gs[2] >= c) lookahead_slots<2, 3>(NX, S, fb, fa, ao, c, nk);
+        } else if (ns == 2) {
+          if (gs[0] >= c) lookahead_slots<0, 2>(NX, S, fb, fa, ao, c, nk);
+          else if (gs[1] >= c) lookahead_slots<1, 2>(NX, S, fb, fa, ao, c, nk);
+        } else if (gs[0] >= c) {
+          lookahead_slots<0, 1>(NX, S, fb, fa, ao, c, nk);
         }
-        if (tw == nd && jb + 1 < gn) {
-          const bool ns = jb + 1 >= 8;
-          Xp[wofs] = ns ? X[1][0] : X[0][0];
-          Xp[wofs + 32] = ns ? X[1][1] : X[0][1];
+        // ---- hand row jb + 2's tiles (jb+2, jb+1) and -(jb+2, jb+2) to the chain
+        if (bw == c % 6) {
+          const int so = c / 6, mo = ((jb + 1) & 1) * 128 + lane;
+          Mb[mo] = so == 0 ? P[0][0] : (so == 1 ? P[1][0] : P[2][0]);
+          Mb[mo + 32] = so == 0 ? P[0][1] : (so == 1 ? P[1][1] : P[2][1]);
+          Mb[mo + 64] = so == 0 ? NX[0][0] : (so == 1 ? NX[1][0] : NX[2][0]);
+          Mb[mo + 96] = so == 0 ? NX[0][1] : (so == 1 ? NX[1][1] : NX[2][1]);
+          __syncwarp();
+          bar_arrive_n<64>(5 + (par ^ 1));
         }
-      }
-      __syncwarp();
-      if (fail >= 0 || jb + 1 == gn) {
-        bar_arrive_all(3 + par);
-        step += jb + 1;
-        break;
-      }
-      // ---- column block jb + 1: P = -(NX + X * X(jb+1)^T)
-      double xb0, xb1;
-      if (tw == nd) {
-        // owner of row jb + 1: straight on to its diagonal tile
-        bar_arrive_all(3 + par);
-        const bool ns = jb + 1 >= 8;
-        xb0 = ns ? X[1][0] : X[0][0];
-        xb1 = ns ? X[1][1] : X[0][1];
-      } else {
-        bar_sync_all(3 + par);
-        // look-ahead this warp deferred while it owned the chain (column jb + 1)
-        if (tw == d && jb > 0) {
-          const int c = jb + 1, fb = tri_frag(t, c, 0, lane), nk = 2 * (c - 1);
-          if (g0 >= c && s1) lookahead_slots<true, true>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
-          else if (s1) lookahead_slots<false, true>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
-          else if (g0 >= c) lookahead_slots<true, false>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
-        }
-        xb0 = Xp[wofs];
-        xb1 = Xp[wofs + 32];
-      }
-      if (s0) {
-        dmma(NX[0], X[0][0], xb0);
-        dmma(NX[0], X[0][1], xb1);
-        P[0][0] = dneg(NX[0][0]), P[0][1] = dneg(NX[0][1]);
-      }
-      if (s1) {
-        dmma(NX[1], X[1][0], xb0);
-        dmma(NX[1], X[1][1], xb1);
-        P[1][0] = dneg(NX[1][0]), P[1][1] = dneg(NX[1][1]);
-      }
-      // ---- look-ahead: column block jb + 2 over the solved blocks 0..jb
-      if (tw != nd && jb + 2 < gn) {
-        const int c = jb + 2, fb = tri_frag(t, c, 0, lane), nk = 2 * (c - 1);
-        const bool a0 = g0 >= c, a1 = has1 && g1 >= c;
-        if (a0 && a1) lookahead_slots<true, true>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
-        else if (a1) lookahead_slots<false, true>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
-        else if (a0) lookahead_slots<true, false>(NX, S, fb, fa0, fa1, ao0, ao1, c, nk);
       }
     }
     __syncthreads();
+    const int fail = flagv[16];
+    step += flagv[16] >= 0 ? (unsigned)(flagv[16] / 8 + 1) : (unsigned)gn;
     // ---- write back the lower triangle (or, on failure, exactly what the
     // reference's block-row order would have stored, ccore.pyx:884-899)
     double *D = g.D.item(b);
@@ -319,7 +355,7 @@ bool potrf_chain_ok(const PotrfArgs &g) {
 
 cudaError_t run_potrf_chain(const PotrfArgs &g, cudaStream_t st) {
   const ix gn = (g.n + 7) / 8;
-  const size_t smem = sizeof(double) * (32 * gn * (gn + 1) + 8 * gn + 128 + 128) + sizeof(uint64_t) + 16 * sizeof(int);
+  const size_t smem = sizeof(double) * (32 * gn * (gn + 1) + 8 * gn + 128 + 128 + 256) + sizeof(uint64_t) + 28 * sizeof(int);
   static LaunchCache cache;
   const int occ = cache.occupancy((const void *)potrf_chain_kernel, CHAIN_THREADS, smem);
   ix grid = (ix)num_sms() * occ;

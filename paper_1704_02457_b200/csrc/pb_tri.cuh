@@ -140,6 +140,57 @@ __device__ __forceinline__ int factor_inv_tile(double (&x)[2], double (&w)[2], i
   return fail;
 }
 
+// 1/d to ~1 ulp: MUFU seed (rel. error 2^-23) + one cubic step, three dependent FMAs.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fma(-d, r, 1.0);
+  const double p = fma(e, e, e);
+  return fma(r, p, r);
+}
+
+// Same contract as factor_inv_tile, shorter dependency chain (the pivot chain
+// of the n > 64 factorization is latency-bound on exactly this sweep).  The
+// columns stay UNSCALED while they are live (u = L * sqrt(d)): the rank-1
+// update uses the multiplier u[r][c] / d_c, so column c's shuffles do not
+// wait for its pivot's rsqrt and the chain per column is shuffle -> 1/d ->
+// multiplier -> FMA (~85 cycles instead of ~300).  Column c of L and row c of
+// W = L^{-1} take their 1/sqrt(d_c) factor when they become final (V is the
+// unit-triangular inverse of U D^{-1}, forward-substituted with the same
+// multipliers).
+__device__ __forceinline__ int factor_inv_tile_u(double (&x)[2], double (&v)[2], int ncol, double *dinv_out, int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  int fail = -1;
+  v[0] = (fr == 2 * fc) ? 1.0 : 0.0;
+  v[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int h = c >> 1, e = c & 1;
+    const double d = __shfl_sync(0xffffffffu, x[e], 4 * c + h);
+    const double ur = __shfl_sync(0xffffffffu, x[e], 4 * fr + h);
+    const double u0 = __shfl_sync(0xffffffffu, x[e], 8 * fc + h);
+    const double u1 = __shfl_sync(0xffffffffu, x[e], 8 * fc + 4 + h);
+    const double v0 = __shfl_sync(0xffffffffu, v[0], 4 * c + fc);
+    const double v1 = __shfl_sync(0xffffffffu, v[1], 4 * c + fc);
+    const bool live = c < ncol && fail < 0;
+    if (live && d <= 0.0) fail = c;  // NaN passes, as in the reference (ccore.pyx:423)
+    const double rc = rcp_nr(d);
+    const double rs = rsqrt_nr(d);
+    if (lane == 0 && live && fail < 0) dinv_out[c] = rs;
+    const double m = ur * rc;
+    // column c of L and row c of W are final: scale them
+    x[e] = fc == h ? x[e] * rs : x[e];
+    v[0] = fr == c ? v[0] * rs : v[0];
+    v[1] = fr == c ? v[1] * rs : v[1];
+    // trailing updates
+    x[0] = 2 * fc > c ? fma(-m, u0, x[0]) : x[0];
+    x[1] = 2 * fc + 1 > c ? fma(-m, u1, x[1]) : x[1];
+    v[0] = fr > c ? fma(-m, v0, v[0]) : v[0];
+    v[1] = fr > c ? fma(-m, v1, v[1]) : v[1];
+  }
+  return fail;
+}
+
 // Store W (from factor_inv_tile) as the B operand of apply_inv_block.
 __device__ __forceinline__ void store_inv_block(const double (&w)[2], double *Wp, int lane) {
   const int fr = lane >> 2, fc = lane & 3;
