@@ -43,20 +43,47 @@ __device__ __forceinline__ double dneg(double x) {
   return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
 }
 
-// NX[s] = -C(g_s, c) + sum_{k-steps < nk} L(g_s, .) L(c, .)^T for slots F..NS-1
-template <int F, int NS>
+// NX[s] = -C(g_s, c) + sum_{k-steps < nk} L(g_s, .) L(c, .)^T for slots F..E-1
+// (nk is even).  A single slot runs two partial accumulators so that its
+// dependent-DMMA latency (26 cycles) stays below the pipe's issue interval.
+template <int F, int E>
 __device__ __forceinline__ void lookahead_slots(double (&NX)[3][2], const double *S, int fb, const int (&fa)[3],
                                                 const int (&ao)[3], int c, int nk) {
 #pragma unroll
-  for (int s = F; s < NS; ++s) {
+  for (int s = F; s < E; ++s) {
     NX[s][0] = dneg(S[ao[s] + 32 * c]);
     NX[s][1] = dneg(S[ao[s] + 32 * c + 4]);
   }
+  if (E - F == 1) {
+    double a1[2] = {0.0, 0.0};
+#pragma unroll 2
+    for (int kk = 0; kk < nk; kk += 2) {
+      dmma(NX[F], S[fa[F] + 16 * kk], S[fb + 16 * kk]);
+      dmma(a1, S[fa[F] + 16 * kk + 16], S[fb + 16 * kk + 16]);
+    }
+    NX[F][0] += a1[0], NX[F][1] += a1[1];
+  } else {
 #pragma unroll 4
-  for (int kk = 0; kk < nk; ++kk) {
-    const double bv = S[fb + 16 * kk];
+    for (int kk = 0; kk < nk; ++kk) {
+      const double bv = S[fb + 16 * kk];
 #pragma unroll
-    for (int s = F; s < NS; ++s) dmma(NX[s], S[fa[s] + 16 * kk], bv);
+      for (int s = F; s < E; ++s) dmma(NX[s], S[fa[s] + 16 * kk], bv);
+    }
+  }
+}
+
+// runtime slot range [f, e) -> the unrolled instance
+__device__ __forceinline__ void lookahead_range(int f, int e, double (&NX)[3][2], const double *S, int fb,
+                                                const int (&fa)[3], const int (&ao)[3], int c, int nk) {
+  if (f == 0) {
+    if (e == 3) lookahead_slots<0, 3>(NX, S, fb, fa, ao, c, nk);
+    else if (e == 2) lookahead_slots<0, 2>(NX, S, fb, fa, ao, c, nk);
+    else if (e == 1) lookahead_slots<0, 1>(NX, S, fb, fa, ao, c, nk);
+  } else if (f == 1) {
+    if (e == 3) lookahead_slots<1, 3>(NX, S, fb, fa, ao, c, nk);
+    else if (e == 2) lookahead_slots<1, 2>(NX, S, fb, fa, ao, c, nk);
+  } else if (f == 2 && e == 3) {
+    lookahead_slots<2, 3>(NX, S, fb, fa, ao, c, nk);
   }
 }
 
@@ -88,7 +115,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
   double *dinv = S + 32 * gn * (gn + 1);                    // cn8 reciprocals
   double *Wp = dinv + t.cn8;                                // 2 x 64: inverted diagonal block, lane-linear
   double *Xp = Wp + 128;                                    // 2 x 64: solved tile (j+1, j), lane-linear
-  double *Mb = Xp + 128;                                    // 2 x 128: hand-off of row j+1's two chain tiles
+  double *Yp = Xp + 128;                                    // 2 x 64: solved tile (j+2, j), lane-linear
+  double *Mb = Yp + 128;                                    // 2 x 128: hand-off of row j+1's two chain tiles
   uint64_t *tbar = reinterpret_cast<uint64_t *>(Mb + 256);  // bulk-load barrier
   volatile int *flagv = reinterpret_cast<volatile int *>(tbar + 1);  // failing column per step (16) + item (1)
 
@@ -220,17 +248,21 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
       // next item's lower panel prefixes into L2 while this one is factored
       if (bw == 5 && nb < g.batch && 4 * lane < n)
         prefetch_l2(g.C.item(nb) + eo(g.ci + 4 * lane, g.cj, g.C.cn), 32u * (unsigned)min(4 * lane + 4, n));
-      // P: this warp's tiles of the current column block, fully downdated;
-      // NX: negated partial sums of the next column block (look-ahead)
-      double P[3][2], NX[3][2], X[3][2];
+      // Per row slot: P = tile (g, jb), complete; NA = negated partial sum of
+      // (g, jb+1) and NB of (g, jb+2), both over the column blocks < jb.  Two
+      // columns of look-ahead: what the chain needs next (row jb+2's tiles)
+      // is two 2-DMMA increments away from the step barrier, and the long
+      // downdate loop (column jb+3) has a whole step of slack.
+      double P[3][2], NA[3][2], NB[3][2], X[3][2];
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
         P[s][0] = S[ao[s]], P[s][1] = S[ao[s] + 4];
-        NX[s][0] = dneg(S[ao[s] + 32]), NX[s][1] = dneg(S[ao[s] + 36]);
+        NA[s][0] = dneg(S[ao[s] + 32]), NA[s][1] = dneg(S[ao[s] + 36]);
+        NB[s][0] = dneg(S[ao[s] + 64]), NB[s][1] = dneg(S[ao[s] + 68]);
       }
       if (bw == 1 && gn > 1) {  // hand row 1's tiles to the chain
         Mb[lane] = P[0][0], Mb[lane + 32] = P[0][1];
-        Mb[lane + 64] = NX[0][0], Mb[lane + 96] = NX[0][1];
+        Mb[lane + 64] = NA[0][0], Mb[lane + 96] = NA[0][1];
         __syncwarp();
         bar_arrive_n<64>(5 + (step & 1));
       }
@@ -242,6 +274,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
         const double wb0 = Wp[wofs], wb1 = Wp[wofs + 32];
         // ---- solve X = P * W^T for rows >= jb + 2 (the accumulator IS the A operand)
         const int c = jb + 2;
+        const int f0 = gs[0] >= c ? 0 : (gs[1] >= c ? 1 : (gs[2] >= c ? 2 : 3));  // first active slot (rows ascend)
+        const bool own = bw == c % 6 && c < gn;                                   // this warp owns row jb + 2 (slot f0)
 #pragma unroll
         for (int s = 0; s < 3; ++s)
           if (s < ns && gs[s] >= c) {
@@ -251,38 +285,40 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
             S[ao[s] + 32 * jb] = X[s][0];
             S[ao[s] + 32 * jb + 4] = X[s][1];
           }
+        if (own) {  // tile (jb+2, jb), lane-linear: everyone's B operand for column block jb + 2
+          Yp[wofs] = f0 == 0 ? X[0][0] : (f0 == 1 ? X[1][0] : X[2][0]);
+          Yp[wofs + 32] = f0 == 0 ? X[0][1] : (f0 == 1 ? X[1][1] : X[2][1]);
+        }
         bar_sync_n<STEP_THREADS>(3 + par);
         if (c >= gn) continue;  // nothing below row jb + 1
-        // ---- column block jb + 1: P = -(NX + X * L(jb+1, jb)^T)
+        // ---- block jb into column blocks jb + 1 (complete: P) and jb + 2
         const double xb0 = Xp[wofs], xb1 = Xp[wofs + 32];
+        const double yb0 = Yp[wofs], yb1 = Yp[wofs + 32];
 #pragma unroll
         for (int s = 0; s < 3; ++s)
           if (s < ns && gs[s] >= c) {
-            dmma(NX[s], X[s][0], xb0);
-            dmma(NX[s], X[s][1], xb1);
-            P[s][0] = dneg(NX[s][0]), P[s][1] = dneg(NX[s][1]);
+            dmma(NA[s], X[s][0], xb0);
+            dmma(NA[s], X[s][1], xb1);
+            dmma(NB[s], X[s][0], yb0);
+            dmma(NB[s], X[s][1], yb1);
+            P[s][0] = dneg(NA[s][0]), P[s][1] = dneg(NA[s][1]);
+            NA[s][0] = NB[s][0], NA[s][1] = NB[s][1];
           }
-        // ---- look-ahead: column block jb + 2 over the solved blocks 0..jb
-        const int fb = tri_frag(t, c, 0, lane), nk = 2 * (c - 1);
-        if (ns == 3) {
-          if (gs[0] >= c) lookahead_slots<0, 3>(NX, S, fb, fa, ao, c, nk);
-          else if (gs[1] >= c) lookahead_slots<1, 3>(NX, S, fb, fa, ao, c, nk);
-          else if (gs[2] >= c) lookahead_slots<2, 3>(NX, S, fb, fa, ao, c, nk);
-        } else if (ns == 2) {
-          if (gs[0] >= c) lookahead_slots<0, 2>(NX, S, fb, fa, ao, c, nk);
-          else if (gs[1] >= c) lookahead_slots<1, 2>(NX, S, fb, fa, ao, c, nk);
-        } else if (gs[0] >= c) {
-          lookahead_slots<0, 1>(NX, S, fb, fa, ao, c, nk);
-        }
         // ---- hand row jb + 2's tiles (jb+2, jb+1) and -(jb+2, jb+2) to the chain
-        if (bw == c % 6) {
-          const int so = c / 6, mo = ((jb + 1) & 1) * 128 + lane;
-          Mb[mo] = so == 0 ? P[0][0] : (so == 1 ? P[1][0] : P[2][0]);
-          Mb[mo + 32] = so == 0 ? P[0][1] : (so == 1 ? P[1][1] : P[2][1]);
-          Mb[mo + 64] = so == 0 ? NX[0][0] : (so == 1 ? NX[1][0] : NX[2][0]);
-          Mb[mo + 96] = so == 0 ? NX[0][1] : (so == 1 ? NX[1][1] : NX[2][1]);
+        if (own) {
+          const int mo = ((jb + 1) & 1) * 128 + lane;
+          Mb[mo] = f0 == 0 ? P[0][0] : (f0 == 1 ? P[1][0] : P[2][0]);
+          Mb[mo + 32] = f0 == 0 ? P[0][1] : (f0 == 1 ? P[1][1] : P[2][1]);
+          Mb[mo + 64] = f0 == 0 ? NA[0][0] : (f0 == 1 ? NA[1][0] : NA[2][0]);
+          Mb[mo + 96] = f0 == 0 ? NA[0][1] : (f0 == 1 ? NA[1][1] : NA[2][1]);
           __syncwarp();
           bar_arrive_n<64>(5 + (par ^ 1));
+        }
+        // ---- long look-ahead: column block jb + 3 over the solved blocks 0..jb
+        const int c3 = jb + 3;
+        if (c3 < gn) {
+          const int f3 = gs[0] >= c3 ? 0 : (gs[1] >= c3 ? 1 : (gs[2] >= c3 ? 2 : 3));
+          if (f3 < ns) lookahead_range(f3, ns, NB, S, tri_frag(t, c3, 0, lane), fa, ao, c3, 2 * (jb + 1));
         }
       }
     }
@@ -355,7 +391,7 @@ bool potrf_chain_ok(const PotrfArgs &g) {
 
 cudaError_t run_potrf_chain(const PotrfArgs &g, cudaStream_t st) {
   const ix gn = (g.n + 7) / 8;
-  const size_t smem = sizeof(double) * (32 * gn * (gn + 1) + 8 * gn + 128 + 128 + 256) + sizeof(uint64_t) + 28 * sizeof(int);
+  const size_t smem = sizeof(double) * (32 * gn * (gn + 1) + 8 * gn + 128 + 128 + 128 + 256) + sizeof(uint64_t) + 28 * sizeof(int);
   static LaunchCache cache;
   const int occ = cache.occupancy((const void *)potrf_chain_kernel, CHAIN_THREADS, smem);
   ix grid = (ix)num_sms() * occ;

@@ -178,15 +178,13 @@ __device__ __forceinline__ int factor_inv_tile_u(double (&x)[2], double (&v)[2],
     const double rs = rsqrt_nr(d);
     if (lane == 0 && live && fail < 0) dinv_out[c] = rs;
     const double m = ur * rc;
-    // column c of L and row c of W are final: scale them
-    x[e] = fc == h ? x[e] * rs : x[e];
-    v[0] = fr == c ? v[0] * rs : v[0];
-    v[1] = fr == c ? v[1] * rs : v[1];
+    // column c of L and row c of W are final: scale them (predicated, no selects)
+    if (fc == h) x[e] *= rs;
+    if (fr == c) v[0] *= rs, v[1] *= rs;
     // trailing updates
-    x[0] = 2 * fc > c ? fma(-m, u0, x[0]) : x[0];
-    x[1] = 2 * fc + 1 > c ? fma(-m, u1, x[1]) : x[1];
-    v[0] = fr > c ? fma(-m, v0, v[0]) : v[0];
-    v[1] = fr > c ? fma(-m, v1, v[1]) : v[1];
+    if (2 * fc > c) x[0] = fma(-m, u0, x[0]);
+    if (2 * fc + 1 > c) x[1] = fma(-m, u1, x[1]);
+    if (fr > c) v[0] = fma(-m, v0, v[0]), v[1] = fma(-m, v1, v[1]);
   }
   return fail;
 }
