@@ -21,8 +21,9 @@
 //    column with warp shuffles (pivot broadcast, sqrt, one reciprocal,
 //    column scale, rank-1 update of the panel's remaining columns), then
 //    the trailing lower tiles take  T(i,j) -= P(i) P(j)^T  on DMMA; a panel
-//    tile's A fragment (8x4, row-major) is also the B fragment of its
-//    transpose, so each panel tile is converted once (4 quad shuffles);
+//    tile's accumulator registers are used directly as the A fragment and,
+//    for its transpose, the B fragment (k-step e contracts over columns
+//    2q + e), so the update needs no shuffles;
 //  * no shared memory and no barriers: occupancy is set by registers only,
 //    and other warps hide each item's load latency and pivot chain; the
 //    next item's rows are prefetched into L2 by one bulk prefetch.
@@ -171,23 +172,18 @@ __global__ void __launch_bounds__(32, (GM <= 2 ? 32 : (GM <= 4 ? 16 : (GM <= 6 ?
       }
       dkeep[k] = myinv;  // lane j < 8: 1/L[8k+j][8k+j], written after the finiteness check
       // trailing update  T(i,jj) -= P(i) P(jj)^T,  k < jj <= i
+      // (an accumulator tile IS an m8n8k4 operand when k-step e of a pair
+      // contracts over columns 2q + e: lane (r, q) holds P[r][2q + e] -- the A
+      // element of row r and, for P^T, the B element of column r -- so the
+      // panel tiles feed the DMMAs straight from their registers, no shuffles)
       if (k + 1 < GM) {
-        double a0[GM], a1[GM];
 #pragma unroll
         for (int i = k + 1; i < GM; ++i) {
-          const int s0 = 4 * r + (q >> 1), s1 = s0 + 2;
-          const double x0 = __shfl_sync(FULL, T[ti(i, k)][0], s0), x1 = __shfl_sync(FULL, T[ti(i, k)][1], s0);
-          const double y0 = __shfl_sync(FULL, T[ti(i, k)][0], s1), y1 = __shfl_sync(FULL, T[ti(i, k)][1], s1);
-          a0[i] = (q & 1) ? x1 : x0;  // P(i)[r][q]
-          a1[i] = (q & 1) ? y1 : y0;  // P(i)[r][4 + q]
-        }
-#pragma unroll
-        for (int i = k + 1; i < GM; ++i) {
-          const double na0 = -a0[i], na1 = -a1[i];
+          const double na0 = -T[ti(i, k)][0], na1 = -T[ti(i, k)][1];
 #pragma unroll
           for (int jj = k + 1; jj <= i; ++jj) {
-            dmma(T[ti(i, jj)], na0, a0[jj]);
-            dmma(T[ti(i, jj)], na1, a1[jj]);
+            dmma(T[ti(i, jj)], na0, T[ti(jj, k)][0]);
+            dmma(T[ti(i, jj)], na1, T[ti(jj, k)][1]);
           }
         }
       }
