@@ -38,18 +38,17 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __host__ __device__ constexpr int ti(int i, int j) { return i * (i + 1) / 2 + j; }
 
-// 1/sqrt(d) for the pivot: MUFU seed + two Newton steps (FMA), branch-free;
-// the pivot chain is the kernel's critical path, and __dsqrt_rn +
-// __ddiv_rn cost two slow-path call sequences per column.  d > 0 here
-// (d <= 0 failed before); NaN propagates.
+// 1/sqrt(d) for the pivot: MUFU seed (rel. error 2^-22) + ONE cubic step
+// y (1 + e/2 + 3e^2/8), e = 1 - d y^2: five FP64 instructions instead of the
+// seven of two Newton steps, branch-free (the kernel is bound by its FP64 /
+// issue slots, not by this chain; __dsqrt_rn + __ddiv_rn cost two slow-path
+// call sequences per column).  d > 0 here (d <= 0 failed before); NaN propagates.
 __device__ __forceinline__ double rsqrt_nr(double d) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  const double h = 0.5 * d;
-  double e = fma(-h * y, y, 0.5);
-  y = fma(y, e, y);
-  e = fma(-h * y, y, 0.5);
-  return fma(y, e, y);
+  const double e = fma(-(d * y), y, 1.0);
+  const double p = fma(0.375, e, 0.5);
+  return fma(y, e * p, y);
 }
 
 __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
