@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 OBJ_DIR = os.path.join(HERE, "build")
 LIB_PATH = os.path.join(LIB_DIR, "libpb_b200.so")
-SOURCES = ["pb_capi.cu", "pb_gemm.cu", "pb_factor.cu", "pb_potrf_small.cu", "pb_potrf_reg.cu", "pb_potrf_chain.cu", "pb_exact.cu", "pb_pack.cu", "pb_chain.cu", "pb_getrf.cu"]
+SOURCES = ["pb_capi.cu", "pb_gemm.cu", "pb_factor.cu", "pb_potrf_small.cu", "pb_potrf_reg.cu", "pb_potrf_chain.cu", "pb_trsm_wide.cu", "pb_exact.cu", "pb_pack.cu", "pb_chain.cu", "pb_getrf.cu"]
 HEADERS = ["pb_common.cuh", "pb_gemm.cuh", "pb_tri.cuh", "pb_exact.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]

@@ -640,6 +640,7 @@ cudaError_t run_diag_check(const Mat &A, ix ai, ix aj, ix n, ix batch, int32_t *
 }
 
 cudaError_t run_trsm_rltn(const TrsmArgs &g, cudaStream_t st) {
+  if (trsm_wide_ok(g)) return run_trsm_wide(g, st);  // register-resident strips (pb_trsm_wide.cu)
   // team width: the warps of a team take the item's 8-row strips round-robin
   // and meet at a barrier per item, so pick the width with the best strip
   // utilisation gmr / (TW * rounds) (ties -> wider team, fewer rounds): e.g.

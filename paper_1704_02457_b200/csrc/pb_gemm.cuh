@@ -112,6 +112,8 @@ bool potrf_chain_ok(const PotrfArgs &g);
 cudaError_t run_potrf_chain(const PotrfArgs &g, cudaStream_t st);
 cudaError_t run_potrf_exact_fixup(const PotrfArgs &g, cudaStream_t st);
 bool trsm_fits(ix m, ix n);
+bool trsm_wide_ok(const TrsmArgs &g);
+cudaError_t run_trsm_wide(const TrsmArgs &g, cudaStream_t st);
 size_t getrf_smem(int m, int n);
 cudaError_t run_getrf(int m, int n, int pivot, const Mat &C, ix ci, ix cj, const Mat &D, ix di, ix dj, int64_t *ipiv,
                       ix ipiv_stride, int32_t *info, ix batch, cudaStream_t st);
