@@ -402,10 +402,20 @@ __global__ void potrf_commit_kernel(Mat S, Mat D, ix di, ix dj, ix rows, ix cols
   if (rmax <= 0) return;
   const double *s = S.p + b * S.stride;
   double *d = D.p + b * D.stride;
-  // consecutive threads walk the source panel-major order (4 rows x column)
-  const ix nq = (rmax + 3) / 4, per = nq * cols * 4;
+  // whole 4-row panels of an aligned window are contiguous runs of 32 * cols bytes on both sides: 16-byte copies
+  ix r0 = 0;
+  if (!lower && (di & 3) == 0 && (((uintptr_t)s | (uintptr_t)d) & 15) == 0 && ((S.stride | D.stride) & 1) == 0) {
+    const int nfull = (int)(rmax >> 2), vpp = 2 * (int)cols, nv = nfull * vpp;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+      const int p = v / vpp, o = v - p * vpp;
+      reinterpret_cast<double2 *>(d + eo(di + 4 * p, dj, D.cn))[o] = reinterpret_cast<const double2 *>(s + (ix)4 * p * S.cn)[o];
+    }
+    r0 = (ix)4 * nfull;
+  }
+  // the rest (a partial last panel, unaligned or lower-only windows) element-wise, in the source's panel-major order
+  const ix nq = (rmax - r0 + 3) / 4, per = nq * cols * 4;
   for (ix e = (ix)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (ix)gridDim.x * blockDim.x) {
-    const ix r = (e / (4 * cols)) * 4 + (e & 3), c = (e >> 2) % cols;
+    const ix r = r0 + (e / (4 * cols)) * 4 + (e & 3), c = (e >> 2) % cols;
     if (r >= rmax || (lower && c > r)) continue;
     d[eo(di + r, dj + c, D.cn)] = s[eo(r, c, S.cn)];
   }
