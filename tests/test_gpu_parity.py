@@ -338,7 +338,7 @@ def test_potrf_nonfinite_inputs_keep_reference_pattern(n):
         assert np.allclose(g[fin], w[fin], rtol=1e-11, atol=1e-11), (n, b)
 
 
-@pytest.mark.parametrize("mn", [(12, 8), (40, 24), (72, 48), (30, 64)])
+@pytest.mark.parametrize("mn", [(12, 8), (40, 24), (72, 48), (30, 64), (80, 72)])
 def test_trsm_reuse_after_unchecked_failing_potrf(mn):
     """potrf_l(check=False) with failing items, then trsm_rltn on the factor:
     healthy items reuse diag_inv, failed items recompute 1/A[j,j] like the
@@ -411,7 +411,9 @@ def test_potrf_concurrent_streams_disjoint_items():
 
 
 @pytest.mark.parametrize("mn", [(2, 2), (5, 3), (8, 8), (3, 9), (13, 6), (72, 48), (40, 64), (33, 100), (16, 232),
-                                (24, 256), (9, 300)])
+                                (24, 256), (9, 300),
+                                # register-strip kernel (m >= 64, 64 <= n <= 128, aligned A): full / ragged strips and blocks
+                                (72, 64), (100, 72), (130, 125), (64, 128)])
 def test_trsm_rltn_random_vs_oracle(mn):
     m, n = mn
     rng = np.random.default_rng(m * 3 + n)
@@ -445,8 +447,8 @@ def test_trsm_rltn_random_vs_oracle(mn):
 
 def test_trsm_zero_pivot_leaves_item_untouched():
     rng = np.random.default_rng(3)
-    for n in (4, 48, 256):
-        nb, m = 5, 7
+    for n, m in ((4, 7), (48, 7), (256, 7), (96, 70)):
+        nb = 5
         L = np.linalg.cholesky(spd_batch(rng, nb, n))
         L[2, n // 2, n // 2] = 0.0
         A = rand_batch(rng, nb, n, n)
@@ -526,6 +528,14 @@ def test_aliasing_and_determinism_bit_exact():
         x3 = alloc(nb, 7, m, zero=True)
         level3.trsm_rltn(7, m, 1.0, out, bm, x3)
         assert torch.equal(x1.storage, x3.storage)
+        if m >= 64:  # register-strip trsm kernel (m >= 64 rows): D == B in place, bit for bit
+            bw = pack.panel_from_array(rng.uniform(-1, 1, (nb, 70, m)))
+            y1 = alloc(nb, 70, m, zero=True)
+            level3.trsm_rltn(70, m, 1.0, out, bw, y1)
+            y2 = alloc(nb, 70, m, zero=True)
+            pack.gecp(70, m, bw, y2)
+            level3.trsm_rltn(70, m, 1.0, out, y2, y2)
+            assert torch.equal(y1.storage, y2.storage)
 
 
 def test_broadcast_operand():
@@ -1232,7 +1242,9 @@ def test_guard_bands_potrf_and_trsm(n):
     level3.potrf_l(n, C, C, check=False)
     X, xchk = _guarded(nb, 24, n)
     level3.trsm_rltn(24, n, 1.0, D, X, X, check=False)
-    for ck, w in ((cchk, "C"), (dchk, "D"), (xchk, "X")):
+    Y, ychk = _guarded(nb, 70, n)  # 70 rows: the register-strip trsm kernel for 64 <= n <= 128 (ragged last strip)
+    level3.trsm_rltn(70, n, 1.0, D, Y, Y, check=False)
+    for ck, w in ((cchk, "C"), (dchk, "D"), (xchk, "X"), (ychk, "Y")):
         ck(f"potrf/trsm n={n} {w}")
 
 
