@@ -146,12 +146,15 @@ def syrk_case(rng):
 
 
 def trsm_case(rng):
-    m, n = int(rng.integers(1, 90)), int(rng.integers(1, 70))
-    nb = int(rng.integers(1, 20))
+    wide = rng.random() < 0.3  # the register-strip kernel: m >= 64, 64 <= n <= 128, panel-aligned A
+    m, n = (int(rng.integers(64, 200)), int(rng.integers(64, 129))) if wide else (int(rng.integers(1, 90)), int(rng.integers(1, 70)))
+    nb = int(rng.integers(1, 6 if wide else 20))
     alpha = float(rng.choice([1.0, -1.0, 0.5]))
     g = rng.uniform(-1, 1, (nb, n, n))
     a = np.linalg.cholesky(g @ g.transpose(0, 2, 1) + n * np.eye(n))
     oa, ob, od = ((int(rng.integers(0, 5)), int(rng.integers(0, 3))) for _ in range(3))
+    if wide and rng.random() < 0.8:
+        oa = (4 * int(rng.integers(0, 2)), oa[1])
     A = O.HostBatch(nb, oa[0] + n, oa[1] + n)
     A.storage[:] = rng.uniform(-1, 1, A.storage.shape)
     A.set_window(oa[0], oa[1], a)
