@@ -16,7 +16,9 @@
 //    acc = alpha * B_j - sum_{k<j} X_k L_jk^T ;   X_j = acc * W_jj^T
 // costs one shared-memory load (the L_jk fragment, read with the same
 // permuted k mapping) per DMMA and nothing else; the negated X_k stay in
-// registers for the later column blocks, X_j goes straight to D.  W_jj =
+// registers for the later column blocks (in the slots that held the strip's
+// alpha * B tiles, all requested before the triangle is even staged), X_j
+// goes straight to D.  W_jj =
 // L_jj^{-1} (all diagonal blocks, built once per item by the CTA's warps) is
 // stored lane-linear so its fragment is one conflict-free load.  The strips
 // of an item are independent: 8 warps x 2 CTAs per SM keep 16 accumulator
@@ -32,6 +34,13 @@ constexpr int GNMAX = 16;   // column blocks (n <= 128)
 
 __device__ __forceinline__ double dneg(double x) {
   return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+
+// bytes need not be a multiple of 16 here: round down, the tail comes with the first demand load
+__device__ __forceinline__ void prefetch_l2_range(const void *p, int bytes) {
+  const unsigned b16 = (unsigned)bytes & ~15u;
+  if (b16 && ((uintptr_t)p & 15) == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(b16) : "memory");
 }
 
 __global__ void __launch_bounds__(WT, 2) trsm_wide_kernel(TrsmArgs g) {
@@ -60,6 +69,25 @@ __global__ void __launch_bounds__(WT, 2) trsm_wide_kernel(TrsmArgs g) {
   for (ix b = (ix)blockIdx.x; b < g.batch; b += (ix)gridDim.x) {
     if (g.skip && g.skip[b] >= 0) continue;
     tri_load_bulk(S, t, g.A.item(b), g.A.cn, g.ai, g.aj, n, n, gn, tbar, tid, WT);
+    // R: the strip's register file -- tile k holds alpha * B_k until column block k is solved, then -X_k (the A
+    // operand of the later blocks).  The first strip's B tiles are requested now, before the triangle is staged
+    // and its diagonal blocks inverted, so their HBM latency is hidden; later strips are pulled into L2.
+    const double *Bb = g.B.item(b);
+    double *Db = g.D.item(b);
+    double R[GNMAX][2];
+    auto load_strip = [&](int gg) {
+      const int row = 8 * gg + r;
+      const ix offB = eo(g.bi + row, g.bj + 2 * q, g.B.cn);
+#pragma unroll
+      for (int j = 0; j < GNMAX; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          R[j][e] = (j < gn && row < m && 8 * j + 2 * q + e < n) ? Bb[offB + 4 * (8 * j + e)] : 0.0;
+    };
+    if (tw < gmr) load_strip(tw);
+    for (int gg = tw + WT / 32; gg < gmr; gg += WT / 32)
+      if (lane < 2 && 8 * gg + 4 * lane < m)  // the strip's two 4-row panels: contiguous runs of 32 n bytes
+        prefetch_l2_range(Bb + eo(g.bi + 8 * gg + 4 * lane, g.bj, g.B.cn), 32 * n);
     const bool reuse = g.use_dA == 1 || (g.use_dA == 2 && g.info[b] < 0);
     if (tid == 0) *flag = 0x7fffffff;
     mbar_wait(tbar, tphase);
@@ -90,35 +118,22 @@ __global__ void __launch_bounds__(WT, 2) trsm_wide_kernel(TrsmArgs g) {
         for (int e = 0; e < 2; ++e) Wall[64 * jb + 32 * (r & 1) + 4 * (2 * q + e) + (r >> 1)] = x[e];
       }
       __syncthreads();
-      const double *Bb = g.B.item(b);
-      double *Db = g.D.item(b);
       for (int gg = tw; gg < gmr; gg += WT / 32) {
+        if (gg != tw) load_strip(gg);
         const int row = 8 * gg + r;
         const bool rok = row < m;
-        const ix offB = eo(g.bi + row, g.bj + 2 * q, g.B.cn), offD = eo(g.di + row, g.dj + 2 * q, g.D.cn);
-        double NX[GNMAX][2];  // -X_k, the A operands of the later column blocks
-        double bq[3][2];      // alpha * B tiles, loaded three column blocks ahead
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            bq[j][e] = (j < gn && rok && 8 * j + 2 * q + e < n) ? Bb[offB + 4 * (8 * j + e)] : 0.0;
+        const ix offD = eo(g.di + row, g.dj + 2 * q, g.D.cn);
 #pragma unroll
         for (int j = 0; j < GNMAX; ++j) {
           if (j < gn) {
             double acc[2];
-            acc[0] = __dmul_rn(g.alpha, bq[j % 3][0]);
-            acc[1] = __dmul_rn(g.alpha, bq[j % 3][1]);
-            if (j + 3 < GNMAX) {
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                bq[j % 3][e] = (j + 3 < gn && rok && 8 * (j + 3) + 2 * q + e < n) ? Bb[offB + 4 * (8 * (j + 3) + e)] : 0.0;
-            }
+            acc[0] = __dmul_rn(g.alpha, R[j][0]);
+            acc[1] = __dmul_rn(g.alpha, R[j][1]);
             const int lb = 32 * j * (j + 1) + hi * (32 * j + 32) + lbl;
 #pragma unroll
             for (int k = 0; k < j; ++k) {
-              dmma(acc, NX[k][0], S[lb + 32 * k]);
-              dmma(acc, NX[k][1], S[lb + 32 * k + 4]);
+              dmma(acc, R[k][0], S[lb + 32 * k]);
+              dmma(acc, R[k][1], S[lb + 32 * k + 4]);
             }
             double X[2] = {0.0, 0.0};
             dmma(X, acc[0], Wall[64 * j + lane]);
@@ -126,7 +141,7 @@ __global__ void __launch_bounds__(WT, 2) trsm_wide_kernel(TrsmArgs g) {
 #pragma unroll
             for (int e = 0; e < 2; ++e)
               if (rok && 8 * j + 2 * q + e < n) Db[offD + 4 * (8 * j + e)] = X[e];
-            NX[j][0] = dneg(X[0]), NX[j][1] = dneg(X[1]);
+            R[j][0] = dneg(X[0]), R[j][1] = dneg(X[1]);
           }
         }
       }
