@@ -499,6 +499,24 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
     g.tmaC = tma_ok(sC);
     g.skip = info;
     if ((r = finish(run_syrk_ln(g, st)))) return r;
+    // a square trailing block the chain kernel factors in one launch also commits the rows below the
+    // first panel (step 4) per item, right after the item's factorization
+    if (m == n && potrf_direct(m - n1, n - n1)) {
+      PotrfArgs p;
+      p.m = m - n1, p.n = n - n1;
+      p.C = to_mat(&T), p.D = to_mat(sD);
+      p.ci = 0, p.cj = 0, p.di = di + n1, p.dj = dj + n1;
+      p.info = info;
+      p.batch = batch;
+      p.merge = 1;
+      p.info_offset = off + n1;
+      if (potrf_chain_ok(p) && (W.stride & 1) == 0) {
+        p.commit = 1;
+        p.cS = to_mat(&W);
+        p.c_rows = m - n1, p.c_cols = n1, p.c_di = di + n1, p.c_dj = dj;
+        return finish(run_potrf_chain(p, st));
+      }
+    }
     if ((r = potrf_run(m - n1, n - n1, &T, 0, 0, sD, di + n1, dj + n1, info, 1, off + n1, w, st))) return r;
   }
   // 4. commit the rows below the first panel

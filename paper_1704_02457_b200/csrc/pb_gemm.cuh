@@ -45,6 +45,13 @@ struct PotrfArgs {
   int ab_same = 0;
   Mat A{}, B{};
   ix ai = 0, aj = 0, bi = 0, bj = 0, k = 0;
+  // fused commit (blocked driver, chain kernel only): after item b's factorization, rows [0, rmax) x
+  // [0, c_cols) of the aligned panel matrix cS (the solved rows below the previous panel) are copied to
+  // D at (c_di, c_dj); rmax = c_rows for a healthy item, (f & ~3) + 4 for one failing at local pivot f
+  // (the reference's row-panel write set, ccore.pyx:877-905); skipped items commit nothing
+  int commit = 0;
+  Mat cS{};
+  ix c_rows = 0, c_cols = 0, c_di = 0, c_dj = 0;
 };
 
 struct CopyArgs {

@@ -102,6 +102,40 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Blocked driver: the rows below the previous panel (solved into the aligned workspace matrix cS) go to
+// D once item b's fate is known: rows [0, rmax), rmax = c_rows for a healthy item, (f & ~3) + 4 for one
+// failing at local pivot f (the reference's row-panel write set).  Whole 4-row panels are contiguous runs
+// of 32 c_cols bytes on both sides.  Kept out of line: the kernel is at its register cap.
+__device__ __noinline__ void commit_rows(const double *cs, double *cd, int scn, int dcn, int c_di, int c_dj, int c_cols,
+                                        int rmax, int tid) {
+  const int vpp = 2 * c_cols, nv = (rmax >> 2) * vpp;
+  for (int v0 = tid; v0 < nv; v0 += 8 * CHAIN_THREADS) {
+    double2 tmp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int v = v0 + u * CHAIN_THREADS;
+      if (v < nv) {
+        const int p = v / vpp, o = v - p * vpp;
+        tmp[u] = reinterpret_cast<const double2 *>(cs + (ix)4 * p * scn)[o];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int v = v0 + u * CHAIN_THREADS;
+      if (v < nv) {
+        const int p = v / vpp, o = v - p * vpp;
+        reinterpret_cast<double2 *>(cd + eo(c_di + 4 * p, c_dj, dcn))[o] = tmp[u];
+      }
+    }
+  }
+  const int rem = rmax & 3;  // a partial last panel, element-wise
+  for (int e = tid; e < rem * c_cols; e += CHAIN_THREADS) {
+    const int rr = (rmax & ~3) + e % rem, c = e / rem;
+    cd[eo(c_di + rr, c_dj + c, dcn)] = cs[eo(rr, c, scn)];
+  }
+}
+
+template <bool COMMIT>
 __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs g) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, tw = warp_uniform();
@@ -374,8 +408,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 3) potrf_chain_kernel(PotrfArgs
     if (tid == 0 && g.info) g.info[b] = fail >= 0 ? fail + g.info_offset : -1;
     if (lane == 0) bulk_wait_read0();  // S is free once the stores have read it
     __syncthreads();
+    const ix bdone = b;
     b = nb;
     if (b < g.batch) load_item(b);
+    if (COMMIT)  // overlaps the next item's staging
+      commit_rows(g.cS.item(bdone), g.D.item(bdone), (int)g.cS.cn, (int)g.D.cn, (int)g.c_di, (int)g.c_dj, (int)g.c_cols,
+                  fail < 0 ? (int)g.c_rows : min((int)g.c_rows, (fail & ~3) + 4), tid);
   }
   if (lane == 0) bulk_wait0();
 }
@@ -392,12 +430,15 @@ bool potrf_chain_ok(const PotrfArgs &g) {
 cudaError_t run_potrf_chain(const PotrfArgs &g, cudaStream_t st) {
   const ix gn = (g.n + 7) / 8;
   const size_t smem = sizeof(double) * (32 * gn * (gn + 1) + 8 * gn + 128 + 128 + 128 + 256) + sizeof(uint64_t) + 28 * sizeof(int);
-  static LaunchCache cache;
-  const int occ = cache.occupancy((const void *)potrf_chain_kernel, CHAIN_THREADS, smem);
+  // two instances: the fused commit costs the plain factorization registers (it is at its cap)
+  static LaunchCache cache[2];
+  const void *kern = g.commit ? (const void *)potrf_chain_kernel<true> : (const void *)potrf_chain_kernel<false>;
+  const int occ = cache[g.commit ? 1 : 0].occupancy(kern, CHAIN_THREADS, smem);
   ix grid = (ix)num_sms() * occ;
   if (grid > g.batch) grid = g.batch;
   if (grid < 1) grid = 1;
-  potrf_chain_kernel<<<(unsigned)grid, CHAIN_THREADS, smem, st>>>(g);
+  if (g.commit) potrf_chain_kernel<true><<<(unsigned)grid, CHAIN_THREADS, smem, st>>>(g);
+  else potrf_chain_kernel<false><<<(unsigned)grid, CHAIN_THREADS, smem, st>>>(g);
   note_launch();
   return cudaGetLastError();
 }
