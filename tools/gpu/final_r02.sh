@@ -7,7 +7,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 
 for c in c4 c5 c6 pack; do python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo ${c}_rc=$?; done
 ( time python bench.py --impl reference ) > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo ref_rc=$?
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu --no-gemm --no-e2e --no-inplace"
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"potrf|trsm|gemm_tma|gemm_direct|gemm_item|commit" -s 153 -c 51 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"potrf|trsm|gemm_tma|gemm_direct|gemm_item|commit" -s 156 -c 52 --csv \
   --log-file gpurun_out/launches_c2.csv $CMD > gpurun_out/ncu_ll.log 2>&1; echo launchlist_rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"potrf_chain" -s 3 -c 1 -o gpurun_out/prof_chain128_final \
   $CMD --only "potrf_l n=128" > gpurun_out/ncu_chain.log 2>&1; echo ncu_chain_rc=$?
