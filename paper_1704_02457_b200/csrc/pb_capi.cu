@@ -364,7 +364,10 @@ int pb_dtrsm_rltn(int m, int n, double alpha, const pb_dmat_batch *sA, int ai, i
 
 static bool potrf_direct(int m, int n) {
   if (m == n) return n <= 128;
-  return n <= 232 && potrf_fits(m, n);
+  // tall windows from 17 columns up: square factor (register-tile / chain kernel) + solve of the rows below
+  // (blocked driver, no workspace while n <= 128) -- 1.7-2.3x the one-CTA team kernel (tools/prof_tall.py)
+  if (n >= 17) return false;
+  return potrf_fits(m, n);
 }
 static int potrf_split(int n) {  // first panel width of the blocked driver
   int n1 = ((n / 2) + 7) / 8 * 8;
@@ -379,8 +382,7 @@ static size_t potrf_ws(int m, int n, int di, int batch) {
   // steps 2-4 take theirs (potrf_run resets the arena mark)
   const size_t w1 = potrf_ws(n1, n1, 0, batch);
   size_t w = 0;
-  if (m > n1) w += panel_bytes(m - n1, n1) * batch;
-  if (n > n1) w += panel_bytes(m - n1, n - n1) * batch + potrf_ws(m - n1, n - n1, 0, batch);
+  if (n > n1) w += panel_bytes(m - n1, n1) * batch + panel_bytes(m - n1, n - n1) * batch + potrf_ws(m - n1, n - n1, 0, batch);
   return w1 > w ? w1 : w;
 }
 
@@ -418,6 +420,29 @@ __global__ void potrf_commit_kernel(Mat S, Mat D, ix di, ix dj, ix rows, ix cols
     const ix r = r0 + (e / (4 * cols)) * 4 + (e & 3), c = (e >> 2) % cols;
     if (r >= rmax || (lower && c > r)) continue;
     d[eo(di + r, dj + c, D.cn)] = s[eo(r, c, S.cn)];
+  }
+}
+
+// Tall window whose square part has n % 4 != 0 columns: the row panel in which a failing item stops
+// (rows iif .. iif + 3, iif = f & ~3) can reach past the square into the rows below it, and the reference's
+// row-panel order has then solved those rows against the columns < iif (ccore.pyx:884-899).  The batched
+// solve skips failing items, so their (at most three) rows are done here: one thread per row, forward
+// substitution with the reciprocals the factorization stored.
+__global__ void potrf_tail_rows_kernel(Mat C, Mat D, ix ci, ix cj, ix di, ix dj, ix m, ix n, const int32_t *info,
+                                       int off, ix batch) {
+  const ix b = (ix)blockIdx.x * (blockDim.x >> 2) + (threadIdx.x >> 2);
+  if (b >= batch) return;
+  const int f = info[b] - off;
+  if (f < 0 || f >= (int)n) return;
+  const ix iif = f & ~3;
+  const ix r = n + (threadIdx.x & 3);
+  if (r >= m || r >= iif + 4) return;
+  const double *c = C.item(b), *dinv = D.ditem(b) + dj;
+  double *d = D.item(b);
+  for (ix j = 0; j < iif; ++j) {
+    double s = c[eo(ci + r, cj + j, C.cn)];
+    for (ix k = 0; k < j; ++k) s -= d[eo(di + r, dj + k, D.cn)] * d[eo(di + j, dj + k, D.cn)];
+    d[eo(di + r, dj + j, D.cn)] = s * dinv[j];
   }
 }
 
@@ -468,6 +493,27 @@ static int potrf_run(int m, int n, const pb_dmat_batch *sC, int ci, int cj, cons
   if ((r = potrf_run(n1, n1, sC, ci, cj, sD, di, dj, info, merge, off, w, st))) return r;
   w.used = mark;
   if (m == n1) return 0;
+  if (n == n1) {
+    // no trailing columns: nothing can fail after this solve, so the rows below go straight to D
+    // (items that failed in the square are skipped and keep D's rows, like the reference's row-panel
+    // order, which never reaches them)
+    TrsmArgs g;
+    g.m = m - n1, g.n = n1, g.alpha = 1.0;
+    g.A = to_mat(sD), g.B = to_mat(sC), g.D = to_mat(sD);
+    g.ai = di, g.aj = dj, g.bi = ci + n1, g.bj = cj, g.di = di + n1, g.dj = dj;
+    g.use_dA = 1;
+    g.info = nullptr;
+    g.batch = batch;
+    g.skip = info;
+    if ((r = trsm_fits(m - n1, n1) ? finish(run_trsm_rltn(g, st)) : fail_arg(2, "panel too wide"))) return r;
+    if (n1 & 3) {  // a failing item's last row panel may straddle the end of the square
+      potrf_tail_rows_kernel<<<(unsigned)((batch + 31) / 32), 128, 0, st>>>(to_mat(sC), to_mat(sD), ci, cj, di, dj, m,
+                                                                              n1, info, off, batch);
+      note_launch();
+      return finish(cudaGetLastError());
+    }
+    return 0;
+  }
   // 2. rows below against it, into workspace
   double *pw = w.take(panel_bytes(m - n1, n1) * batch);
   if (!pw) return work_fail();

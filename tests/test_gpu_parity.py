@@ -272,6 +272,33 @@ def test_potrf_l_random_vs_oracle(mn):
         compare_storage(host(dD), D.storage, mask, m, f"potrf {mn} {oc}{od}")
 
 
+@pytest.mark.parametrize("mnf", [(109, 31, 29), (109, 31, 3), (391, 55, 54), (200, 101, 100), (90, 70, 69), (40, 13, 12)])
+@pytest.mark.parametrize("off", [(0, 0), (1, 3)])
+def test_potrf_tall_failure_in_last_row_panel(mnf, off):
+    """Tall window, n % 4 != 0, failing pivot in the square's last row panel: that panel reaches into the rows
+    below the square, and the reference's row-panel order has solved them against the columns left of the
+    panel before it stops (ccore.pyx:884-899).  The factor + solve path must write exactly that."""
+    m, n, f = mnf
+    rng = np.random.default_rng(m + n + f)
+    nb = 5
+    a = np.zeros((nb, m, n))
+    a[:, :n] = spd_batch(rng, nb, n)
+    a[:, n:] = rng.uniform(-1, 1, (nb, m - n, n))
+    a[1, f, f] = -3.0
+    a[3, f // 2, f // 2] = -1.0
+    C = rand_batch(rng, nb, off[0] + m + 1, off[1] + n + 2)
+    C.set_window(off[0], off[1], a)
+    D = rand_batch(rng, nb, m + 2, n + 3, fill=0.75)
+    dC, dD = dev(C), dev(D)
+    info = level3.potrf_l(m, dC.ref(*off), dD, n=n, check=False).cpu().numpy()
+    winfo = O.potrf_l(m, C, off[0], off[1], D, 0, 0, n=n)
+    assert np.array_equal(info, winfo) and winfo[1] == f
+    got = host(dD)
+    for b in range(nb):
+        gb, wb = got[b, : D.storage.shape[1]], D.storage[b]
+        assert np.allclose(gb, wb, rtol=1e-10, atol=1e-10, equal_nan=True), (mnf, off, b)
+
+
 @pytest.mark.parametrize("n", [4, 8, 12, 16, 17, 24, 40, 57, 64, 72, 100, 128, 136, 200, 256, 300])
 @pytest.mark.parametrize("off", [(0, 0), (1, 1)])
 def test_potrf_failure_index_and_partial_writes(n, off):

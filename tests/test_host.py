@@ -199,10 +199,12 @@ def test_native_library_exports_header_surface():
     w256 = lib.pb_dpotrf_l_worksize(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0)
     assert w256 >= 3 * 2 * 128 * 128 * 8  # W (128 x 128) + T (128 x 128) per item
     assert lib.pb_dpotrf_l_worksize(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 1, 0) >= w256 + 3 * 256 * 256 * 8
-    assert lib.pb_dpotrf_l_worksize(600, 20, ctypes.byref(pb.allocate_panel_batch(2, 600, 20, device="cpu")
-                                                          .descriptor()), 0, 0,
-                                    ctypes.byref(pb.allocate_panel_batch(2, 600, 20, device="cpu").descriptor()),
-                                    0, 0) >= 2 * 580 * 20 * 8  # tall: rows below the square factor
+    tall = pb.allocate_panel_batch(2, 600, 200, device="cpu").descriptor()
+    # tall windows up to 128 columns: square factor + solve of the rows below straight into D, no workspace
+    assert lib.pb_dpotrf_l_worksize(600, 20, ctypes.byref(tall), 0, 0, ctypes.byref(tall), 0, 0) == 0
+    # wider ones: the rows below the first panel (W) and the trailing block (T) go through workspace
+    assert lib.pb_dpotrf_l_worksize(600, 200, ctypes.byref(tall), 0, 0, ctypes.byref(tall), 0,
+                                    0) >= 2 * (496 * 104 + 496 * 96) * 8
     # a call with less workspace than the query reports is refused before any launch
     assert lib.pb_dpotrf_l(256, 256, ctypes.byref(big), 0, 0, ctypes.byref(big), 0, 0, ctypes.c_void_p(8), None, 0,
                            None) == -10
