@@ -612,7 +612,11 @@ static bool syrk_potrf_fused(int m, int n, int k, const pb_dmat_batch *sA, int a
   // squares the register-resident small potrf covers keep its rounding
   // (zero factors then reproduce potrf_l bit for bit, test_level3.py:632-641)
   const bool small = m == n && n <= 16 && (di & 3) == 0 && tma_ok(sD);
-  return !small && syrk_potrf_fits(m, n, k, ab_same);
+  // one kernel for the register-tile squares (17..64) and for windows below 17 columns; wider or tall
+  // windows go syrk -> workspace -> potrf_l (chain kernel / square factor + solve): 2-3x the fused
+  // one-CTA team kernel from 65 columns up (tools/prof_syrk_potrf.py)
+  const bool one_kernel = n <= 16 || (m == n && n <= 64);
+  return !small && one_kernel && syrk_potrf_fits(m, n, k, ab_same);
 }
 
 static int syrk_potrf_check(int m, int n, int k, const pb_dmat_batch *sA, int ai, int aj, const pb_dmat_batch *sB,
