@@ -176,12 +176,14 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
           }
         }
         if (tw == 0) {
-          const int f = factor_diag_tile(acc[0], 8, dinv + 8 * jb, lane);
+          // factor and inverse of the diagonal tile in ONE unscaled column sweep (pb_tri.cuh), instead of
+          // a factor sweep followed by a substitution sweep on the stored tile
+          double wi[2];
+          const int f = factor_inv_tile_u(acc[0], wi, 8, dinv + 8 * jb, lane);
 #pragma unroll
           for (int e = 0; e < 2; ++e) sF[t.off(8 * jb + fr, 8 * jb + 2 * fc + e)] = acc[0][e];
           if (f >= 0 && lane == 0 && *flag < 0) *flag = stage * 1000 + 8 * jb + f;
-          __syncwarp();
-          build_inv_block(sF, t, jb, dinv, 8, Wp + 64 * jb, lane);
+          store_inv_block(wi, Wp + 64 * jb, lane);
         }
 #pragma unroll
         for (int u = 0; u < MAXT; ++u) {

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256, MINB) potrf_team_kernel(PotrfArgs g, int 
           for (int kk = 0; kk < 2 * jb; ++kk) dmma(dg, -S[fb + 16 * kk], S[fb + 16 * kk]);
         }
         double wi[2];
-        const int f = factor_inv_tile(dg, wi, ncol, dinv + 8 * jb, lane);
+        const int f = factor_inv_tile_u(dg, wi, ncol, dinv + 8 * jb, lane);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * fc + e;
