@@ -464,7 +464,13 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
     }
     if (fail < 0) {
       // inverse of every 8x8 diagonal block, spread over the team's warps
-      for (int jb = tw; jb < t.gn; jb += TW) build_inv_block(S, t, jb, dinv, min(8, n - 8 * jb), Wall + 64 * jb, lane);
+      for (int jb = tw; jb < t.gn; jb += TW) {
+        double xl[2], wv[2];
+        xl[0] = S[t.off(8 * jb + fr, 8 * jb + 2 * fc)];
+        xl[1] = S[t.off(8 * jb + fr, 8 * jb + 2 * fc + 1)];
+        inv_tile_regs(xl, dinv + 8 * jb, min(8, n - 8 * jb), wv, lane);
+        store_inv_block(wv, Wall + 64 * jb, lane);
+      }
       team_sync(bar, tthreads);
       const double *B = g.B.item(b);
       double *D = g.D.item(b);

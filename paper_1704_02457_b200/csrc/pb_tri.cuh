@@ -215,6 +215,30 @@ __device__ __forceinline__ void build_inv_block(const double *S, const Tri &t, i
   }
 }
 
+// W = L_jj^{-1} of an already factored 8x8 diagonal block held in REGISTERS (x: accumulator layout, lane
+// (fr, fc) holds L[fr][2fc + e]; dv = 1/L[c][c] for this lane's columns is read from dinv8[0..7]).  Same
+// forward substitution as factor_inv_tile_u's inverse part, but every multiplier L[r][c] / L[c][c] is known
+// up front, so the chain per column is one shuffle + one FMA (~35 cycles) instead of the shared-memory
+// substitution sweep of solve_tile_rt (~150).  w: W in accumulator layout; rows/columns >= ncol stay identity.
+__device__ __forceinline__ void inv_tile_regs(const double (&x)[2], const double *dinv8, int ncol, double (&w)[2], int lane) {
+  const int fr = lane >> 2, fc = lane & 3;
+  w[0] = (fr == 2 * fc) ? 1.0 : 0.0;
+  w[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
+  const double dr = fr < ncol ? dinv8[fr] : 1.0;  // this lane's row scale
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double lr = __shfl_sync(0xffffffffu, x[c & 1], 4 * fr + (c >> 1));  // L[fr][c]
+    const double v0 = __shfl_sync(0xffffffffu, w[0], 4 * c + fc);
+    const double v1 = __shfl_sync(0xffffffffu, w[1], 4 * c + fc);
+    if (c < ncol && fr > c && fr < ncol) {
+      const double m = lr * dinv8[c];
+      w[0] = fma(-m, v0, w[0]);
+      w[1] = fma(-m, v1, w[1]);
+    }
+  }
+  w[0] *= dr, w[1] *= dr;
+}
+
 // acc := X * W^T for an 8x8 tile X held in shared memory (tri layout, rows
 // 8g.., cols 8j..) and W from build_inv_block.
 __device__ __forceinline__ void apply_inv_block(double (&acc)[2], const double *S, const Tri &t, int g, int j,

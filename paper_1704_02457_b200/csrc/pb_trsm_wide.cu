@@ -107,15 +107,15 @@ __global__ void __launch_bounds__(WT, 2) trsm_wide_kernel(TrsmArgs g) {
     __syncthreads();
     const int fail = reuse || *flag == 0x7fffffff ? -1 : *flag;
     if (fail < 0) {
-      // inverse of every 8x8 diagonal block, spread over the warps; W[nn][k] goes to
-      // Wall[64 jb + 32 (k & 1) + 4 nn + (k >> 1)], the B fragment of k-step (k & 1)
+      // inverse of every 8x8 diagonal block, spread over the warps (register sweep, pb_tri.cuh); lane
+      // (nn, q) holds W[nn][2q + e] -- exactly the B fragment of k-step e, so it is stored lane-linear
       for (int jb = tw; jb < gn; jb += WT / 32) {
-        double x[2];
-        x[0] = (r == 2 * q) ? 1.0 : 0.0;
-        x[1] = (r == 2 * q + 1) ? 1.0 : 0.0;
-        solve_tile_rt(x, S, t, jb, dinv, min(8, n - 8 * jb), lane);  // x[k][nn] = Linv[nn][k], k = r, nn = 2q + e
-#pragma unroll
-        for (int e = 0; e < 2; ++e) Wall[64 * jb + 32 * (r & 1) + 4 * (2 * q + e) + (r >> 1)] = x[e];
+        double x[2], wv[2];
+        x[0] = S[t.off(8 * jb + r, 8 * jb + 2 * q)];
+        x[1] = S[t.off(8 * jb + r, 8 * jb + 2 * q + 1)];
+        inv_tile_regs(x, dinv + 8 * jb, min(8, n - 8 * jb), wv, lane);
+        Wall[64 * jb + lane] = wv[0];
+        Wall[64 * jb + 32 + lane] = wv[1];
       }
       __syncthreads();
       for (int gg = tw; gg < gmr; gg += WT / 32) {
