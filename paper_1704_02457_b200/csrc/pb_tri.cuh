@@ -34,67 +34,6 @@ __device__ __forceinline__ int tri_frag(const Tri &t, int g, int kk, int lane) {
   return t.group_off(g) + (lane >> 4) * 4 * t.width(g) + 16 * kk + 4 * (lane & 3) + ((lane >> 2) & 3);
 }
 
-// In-register solve of an 8x8 accumulator tile x (fragment layout: lane
-// holds row lane>>2, cols 2(lane&3)+e) against the lower 8x8 diagonal
-// block L (shared, tri layout at rows/cols 8j..), x <- x * L^{-T}, with
-// reciprocals dinv (shared).  ncol = valid columns in the block.
-__device__ __forceinline__ void solve_tile_rt(double (&x)[2], const double *S, const Tri &t, int j,
-                                              const double *dinv, int ncol, int lane) {
-  const int fr = lane >> 2, fc = lane & 3;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    if (c < ncol) {
-      const double inv = dinv[8 * j + c];
-      if (fc == (c >> 1)) x[c & 1] = __dmul_rn(x[c & 1], inv);
-      const double xc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c2 = 2 * fc + e;
-        if (c2 > c && c2 < ncol) x[e] = fma(-xc, S[t.off(8 * j + c2, 8 * j + c)], x[e]);
-      }
-    }
-  }
-}
-
-// Right-looking in-register Cholesky of the 8x8 diagonal tile (fragment
-// layout).  Returns the first failing column (d <= 0) or -1.  On return the
-// tile holds L for columns < the failing one; dinv_out[c] = 1/L[c,c].
-__device__ __forceinline__ int factor_diag_tile(double (&x)[2], int ncol, double *dinv_out, int lane) {
-  const int fr = lane >> 2, fc = lane & 3;
-  int fail = -1;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    if (c < ncol && fail < 0) {
-      const double d = __shfl_sync(0xffffffffu, x[c & 1], c * 4 + (c >> 1));
-      if (d <= 0.0) {
-        fail = c;
-      } else {
-        const double inv = rsqrt(d);  // 1/L[c,c] (<= 1 ulp), one MUFU + Newton
-        const double ljj = d * inv;
-        if (fc == (c >> 1)) {
-          if (fr == c) x[c & 1] = ljj;
-          else if (fr > c) x[c & 1] = __dmul_rn(x[c & 1], inv);
-        }
-        if (lane == 0) dinv_out[c] = inv;
-        const double lrc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
-        const double l0 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc) * 4 + (c >> 1));
-        const double l1 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc + 1) * 4 + (c >> 1));
-        if (2 * fc > c) x[0] = fma(-lrc, l0, x[0]);
-        if (2 * fc + 1 > c) x[1] = fma(-lrc, l1, x[1]);
-      }
-    }
-  }
-  return fail;
-}
-
-
-// Cholesky factor AND inverse of the 8x8 diagonal tile in one column sweep
-// (fragment layout: lane holds row lane>>2, cols 2(lane&3)+e).  Column c:
-// one shuffle for the pivot, rsqrt, scale, three shuffles for the rank-1
-// update of the trailing tile; the inverse W = L^{-1} is forward-substituted
-// in the same sweep (row c of W scaled by 1/L[c,c], rows below updated),
-// so its chain overlaps the factor's.  Returns the first failing column or
-// -1; dinv_out[c] = 1/L[c,c]; W's rows/cols past ncol are unused.
 // 1/sqrt(d) to ~1 ulp: MUFU seed + two Newton steps, branch-free (the
 // library rsqrt() carries special-case paths that break warp convergence).
 __device__ __forceinline__ double rsqrt_nr(double d) {
@@ -106,40 +45,6 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return y;
 }
 
-__device__ __forceinline__ int factor_inv_tile(double (&x)[2], double (&w)[2], int ncol, double *dinv_out, int lane) {
-  const int fr = lane >> 2, fc = lane & 3;
-  int fail = -1;
-  w[0] = (fr == 2 * fc) ? 1.0 : 0.0;
-  w[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
-  // Branch-free sweep (every lane runs every column; the pivot test only
-  // records the first failure -- values past it are never stored).
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double d = __shfl_sync(0xffffffffu, x[c & 1], c * 4 + (c >> 1));
-    const bool live = c < ncol && fail < 0;
-    if (live && d <= 0.0) fail = c;  // NaN passes, as in the reference (ccore.pyx:423)
-    const double inv = rsqrt_nr(d);
-    const bool own = fc == (c >> 1);
-    const double xs = x[c & 1];
-    x[c & 1] = own && fr == c ? d * inv : (own && fr > c ? __dmul_rn(xs, inv) : xs);
-    if (fr == c) {
-      w[0] = __dmul_rn(w[0], inv);
-      w[1] = __dmul_rn(w[1], inv);
-    }
-    if (lane == 0 && live && fail < 0) dinv_out[c] = inv;
-    const double lrc = __shfl_sync(0xffffffffu, x[c & 1], fr * 4 + (c >> 1));
-    const double l0 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc) * 4 + (c >> 1));
-    const double l1 = __shfl_sync(0xffffffffu, x[c & 1], (2 * fc + 1) * 4 + (c >> 1));
-    const double wc0 = __shfl_sync(0xffffffffu, w[0], c * 4 + fc);
-    const double wc1 = __shfl_sync(0xffffffffu, w[1], c * 4 + fc);
-    x[0] = 2 * fc > c ? fma(-lrc, l0, x[0]) : x[0];
-    x[1] = 2 * fc + 1 > c ? fma(-lrc, l1, x[1]) : x[1];
-    w[0] = fr > c ? fma(-lrc, wc0, w[0]) : w[0];
-    w[1] = fr > c ? fma(-lrc, wc1, w[1]) : w[1];
-  }
-  return fail;
-}
-
 // 1/d to ~1 ulp: MUFU seed (rel. error 2^-23) + one cubic step, three dependent FMAs.
 __device__ __forceinline__ double rcp_nr(double d) {
   double r;
@@ -149,12 +54,16 @@ __device__ __forceinline__ double rcp_nr(double d) {
   return fma(r, p, r);
 }
 
-// Same contract as factor_inv_tile, shorter dependency chain (the pivot chain
-// of the n > 64 factorization is latency-bound on exactly this sweep).  The
+// Cholesky factor AND inverse of the 8x8 diagonal tile in one column sweep
+// (fragment layout: lane holds row lane>>2, cols 2(lane&3)+e).  Returns the
+// first failing column (d <= 0, NaN passes) or -1; the tile holds L for the
+// columns left of it; dinv_out[c] = 1/L[c,c]; w = W = L^{-1} (rows/cols past
+// ncol unused).  The pivot chain of the n > 64 factorization is latency-bound
+// on exactly this sweep, so its dependency chain is kept short: the
 // columns stay UNSCALED while they are live (u = L * sqrt(d)): the rank-1
 // update uses the multiplier u[r][c] / d_c, so column c's shuffles do not
 // wait for its pivot's rsqrt and the chain per column is shuffle -> 1/d ->
-// multiplier -> FMA (~85 cycles instead of ~300).  Column c of L and row c of
+// multiplier -> FMA (tools/factor_lat.cu: 1140 cycles per tile alone on an SM).  Column c of L and row c of
 // W = L^{-1} take their 1/sqrt(d_c) factor when they become final (V is the
 // unit-triangular inverse of U D^{-1}, forward-substituted with the same
 // multipliers).
@@ -189,37 +98,20 @@ __device__ __forceinline__ int factor_inv_tile_u(double (&x)[2], double (&v)[2],
   return fail;
 }
 
-// Store W (from factor_inv_tile) as the B operand of apply_inv_block.
+// Store W (accumulator layout, from factor_inv_tile_u / inv_tile_regs) as the B operand of
+// apply_inv_block: panel layout, element (n, k) at (n>>2)*32 + 4k + (n&3), read back as the B
+// fragment of an m8n8k4 MMA:  X * L_jj^{-T} = X * W^T.
 __device__ __forceinline__ void store_inv_block(const double (&w)[2], double *Wp, int lane) {
   const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
   for (int e = 0; e < 2; ++e) Wp[(fr >> 2) * 32 + 4 * (2 * fc + e) + (fr & 3)] = w[e];
 }
 
-// W = L_jj^{-1} of the 8x8 diagonal block (rows/cols 8j..), written to Wp in
-// panel layout (element (n, k) at (n>>2)*32 + 4k + (n&3)) so that it is read
-// back as the B operand of an m8n8k4 MMA:  X * L_jj^{-T} = X * W^T.  Built by
-// solving the identity against L_jj in registers (one warp, 8 serial steps);
-// columns past ncol stay identity.
-__device__ __forceinline__ void build_inv_block(const double *S, const Tri &t, int j, const double *dinv, int ncol,
-                                                double *Wp, int lane) {
-  const int fr = lane >> 2, fc = lane & 3;
-  double x[2];
-  x[0] = (fr == 2 * fc) ? 1.0 : 0.0;
-  x[1] = (fr == 2 * fc + 1) ? 1.0 : 0.0;
-  solve_tile_rt(x, S, t, j, dinv, ncol, lane);  // x = I * L^{-T}: x[r][c] = Linv[c][r]
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const int n = 2 * fc + e, k = fr;
-    Wp[(n >> 2) * 32 + 4 * k + (n & 3)] = x[e];
-  }
-}
-
 // W = L_jj^{-1} of an already factored 8x8 diagonal block held in REGISTERS (x: accumulator layout, lane
 // (fr, fc) holds L[fr][2fc + e]; dv = 1/L[c][c] for this lane's columns is read from dinv8[0..7]).  Same
 // forward substitution as factor_inv_tile_u's inverse part, but every multiplier L[r][c] / L[c][c] is known
 // up front, so the chain per column is one shuffle + one FMA (~35 cycles) instead of the shared-memory
-// substitution sweep of solve_tile_rt (~150).  w: W in accumulator layout; rows/columns >= ncol stay identity.
+// substitution sweep it replaces (~150).  w: W in accumulator layout; rows/columns >= ncol stay identity.
 __device__ __forceinline__ void inv_tile_regs(const double (&x)[2], const double *dinv8, int ncol, double (&w)[2], int lane) {
   const int fr = lane >> 2, fc = lane & 3;
   w[0] = (fr == 2 * fc) ? 1.0 : 0.0;
@@ -240,7 +132,7 @@ __device__ __forceinline__ void inv_tile_regs(const double (&x)[2], const double
 }
 
 // acc := X * W^T for an 8x8 tile X held in shared memory (tri layout, rows
-// 8g.., cols 8j..) and W from build_inv_block.
+// 8g.., cols 8j..) and W from store_inv_block.
 __device__ __forceinline__ void apply_inv_block(double (&acc)[2], const double *S, const Tri &t, int g, int j,
                                                 const double *Wp, int lane) {
   const int fr = lane >> 2, fc = lane & 3;

@@ -7,6 +7,8 @@ using namespace pb;
 template <int MODE>
 __global__ void k(double *out, long long *t, int reps, int nactive) {
   __shared__ double dinv[12][8];
+  if (threadIdx.x < 96) dinv[threadIdx.x / 8][threadIdx.x % 8] = 0.3;
+  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, fr = lane >> 2, fc = lane & 3;
   if ((w & 3) != 0 || (w >> 2) >= nactive) return;
   double x0[2], wv[2];
@@ -15,8 +17,8 @@ __global__ void k(double *out, long long *t, int reps, int nactive) {
   long long a = clock64();
   for (int i = 0; i < reps; ++i) {
     double x[2] = {x0[0] + acc * 1e-300, x0[1]};
-    if (MODE == 0) factor_inv_tile(x, wv, 8, dinv[w], lane);
-    else factor_inv_tile_u(x, wv, 8, dinv[w], lane);
+    if (MODE == 0) inv_tile_regs(x, dinv[w], 8, wv, lane);  // inverse of a given factor (trsm kernels)
+    else factor_inv_tile_u(x, wv, 8, dinv[w], lane);        // factor + inverse (potrf chain)
     acc += x[0] + wv[1];
   }
   long long b = clock64();
@@ -30,7 +32,7 @@ int main() {
     for (int r = 0; r < 2; ++r) { k<0><<<1, 384>>>(out, t, 64, na); cudaDeviceSynchronize(); }
     long long t0 = t[0];
     for (int r = 0; r < 2; ++r) { k<1><<<1, 384>>>(out, t, 64, na); cudaDeviceSynchronize(); }
-    printf("%d warp(s) on one scheduler: factor_inv_tile %lld clk, factor_inv_tile_u %lld clk (%s)\n", na, t0, t[0], cudaGetErrorString(cudaGetLastError()));
+    printf("%d warp(s) on one scheduler: inv_tile_regs %lld clk, factor_inv_tile_u %lld clk (%s)\n", na, t0, t[0], cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
