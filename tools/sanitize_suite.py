@@ -32,7 +32,7 @@ def exact(nb, m, n, layout="split"):
 
 def run():
     done = []
-    # potrf: n <= 8 (small1), 16 (quad), 17..64 (register tile + exact pass), 65..128 (team),
+    # potrf: n <= 8 (small1), 16 (quad), 17..64 (register tile + exact pass), 65..128 (chain kernel),
     # 256 / 300 (blocked: trsm + syrk trapezoid + commit), tall windows, unaligned D, failing items
     for n, nb in ((4, 300), (8, 200), (16, 100), (24, 64), (64, 32), (100, 8), (128, 6), (256, 3), (300, 2)):
         for layout in ("split", "interleaved"):
@@ -46,7 +46,7 @@ def run():
             level3.potrf_l(n, C, D, check=False)
             level3.potrf_l(n, C, C, check=False)  # in place
         done.append(f"potrf n={n}")
-    for m, n in ((300, 264), (320, 240), (600, 20), (520, 40)):
+    for m, n in ((300, 264), (320, 240), (600, 20), (520, 40), (256, 128), (109, 31)):  # tall: square factor + solve
         a = torch.from_numpy(rng.uniform(-1, 1, (2, m, n))).cuda()
         a[:, :n, :] = spd(2, n)
         C = exact(2, m, n)
@@ -71,7 +71,7 @@ def run():
         level3.syrk_ln(m, k, -1.0, A.ref(3, 0), A.ref(3, 0), beta, exact(nb, m, m), S)
         done.append(f"gemm/syrk {m}x{n}x{k}")
     # trsm (team widths), blocked trsm (n > team), gemm_nn, trmm in place (workspace), syrk_potrf fused / split
-    for m, n in ((72, 48), (9, 300), (40, 64)):
+    for m, n in ((72, 48), (9, 300), (40, 64), (130, 125), (64, 128)):  # the last two: register-strip kernel
         L = exact(4, n, n)
         Cs = exact(4, n, n)
         pack.pack_array_into(spd(4, n), Cs)
