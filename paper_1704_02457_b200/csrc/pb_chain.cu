@@ -34,10 +34,14 @@ struct ChainCfg {
   static constexpr int TRI = 32 * NB * (NB + 1);  // Tri::size(ns, ns)
   static constexpr int OFF_BAT = 0;                // full panel layout ns x nx
   static constexpr int OFF_RQ = OFF_BAT + NS * NX;  // tri
-  static constexpr int OFF_P = OFF_RQ + TRI;        // full nx x nx
-  static constexpr int OFF_W = OFF_P + NX * NX;     // full ns x nx
-  static constexpr int OFF_F = OFF_W + NS * NX;     // tri
-  static constexpr int OFF_DINV = OFF_F + TRI;      // ns
+  // P (full nx x nx), W (full ns x nx) and F (tri) are never live together once every step accumulates its
+  // tiles in registers and stores them behind a team barrier: ONE buffer holds whichever is current.  31 KB
+  // per problem instead of 47 (nx = 32): seven problems per SM, so Config 5's 1024 problems run in one wave.
+  static constexpr int XSZ = NS * NX > TRI ? NS * NX : TRI;
+  static constexpr int OFF_P = OFF_RQ + TRI;
+  static constexpr int OFF_W = OFF_P;
+  static constexpr int OFF_F = OFF_P;
+  static constexpr int OFF_DINV = OFF_P + XSZ;      // ns
   static constexpr int OFF_WP = OFF_DINV + NS;      // NB inverted diagonal blocks
   static constexpr int OFF_FLAG = OFF_WP + 64 * NB;
   static constexpr int TEAM = (OFF_FLAG + 8 + 15) / 16 * 16;
@@ -51,7 +55,7 @@ __device__ __forceinline__ int full_frag(int g, int kk, int cn, int lane) {
 __device__ __forceinline__ int full_off(int r, int c, int cn) { return (r >> 2) * 4 * cn + 4 * c + (r & 3); }
 
 template <int NXB, int TW>
-__global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
+__global__ void __launch_bounds__(128, (NXB == 4 && TW == 4) ? 7 : 1) chain_kernel(ChainArgs g) {
   using Cfg = ChainCfg<NXB, TW>;
   constexpr int NB = Cfg::NB, NS = Cfg::NS, NX = Cfg::NX;
   extern __shared__ __align__(128) double smem[];
@@ -62,6 +66,10 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
   const int bar = 1 + team;
   const int fr = lane >> 2, fc = lane & 3;
   double *T = smem + (ix)team * Cfg::TEAM;
+  // One team per CTA (launch_chain): the team barrier is the CTA barrier.  A runtime named-barrier id makes
+  // ptxas reserve all 16 hardware barriers for the CTA, which alone caps the SM at 4 CTAs (ncu:
+  // launch__occupancy_limit_barriers).
+  auto team_sync = [&](int, int) { __syncthreads(); };
   double *sBAt = T + Cfg::OFF_BAT, *sRQ = T + Cfg::OFF_RQ, *sP = T + Cfg::OFF_P, *sW = T + Cfg::OFF_W;
   double *sF = T + Cfg::OFF_F, *dinv = T + Cfg::OFF_DINV, *Wp = T + Cfg::OFF_WP;
   volatile int *flag = (volatile int *)(T + Cfg::OFF_FLAG);
@@ -117,6 +125,7 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
             }
           }
         }
+        team_sync(bar, tthreads);  // W replaces P in the shared buffer: every warp is done reading P
 #pragma unroll
         for (int q = 0; q < NT1; ++q) {
           const int tile = tw + q * TW;
@@ -151,6 +160,7 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
           for (int q = 0; q < NT2; ++q)
             if (tw + q * TW < NL) dmma(acc[q], sW[full_frag(ti[q], kk, NX, lane)], sBAt[full_frag(tj[q], kk, NX, lane)]);
         }
+        team_sync(bar, tthreads);  // F replaces W in the shared buffer
 #pragma unroll
         for (int q = 0; q < NT2; ++q)
           if (tw + q * TW < NL) {
@@ -216,24 +226,41 @@ __global__ void __launch_bounds__(128) chain_kernel(ChainArgs g) {
           for (int e = 0; e < 2; ++e) gK[eo(8 * i + fr, 2 * fc + e, g.K.cn)] = -acc[e];
         }
       }
-      // (5) P = Lcal * Lcal^T, Lcal = F[nu:, nu:] (strict upper of its diagonal tiles masked)
-      for (int tile = tw; tile < NXB * NXB; tile += TW) {
-        const int i = tile / NXB, j = tile % NXB;
-        double acc[2] = {0.0, 0.0};
-        const int kbmax = i < j ? i : j;
-        for (int kb = 0; kb <= kbmax; ++kb) {
-          const int fa = tri_frag(t, 1 + i, 0, lane) + 32 * (1 + kb), fb = tri_frag(t, 1 + j, 0, lane) + 32 * (1 + kb);
+      // (5) P = Lcal * Lcal^T, Lcal = F[nu:, nu:] (strict upper of its diagonal tiles masked); the warp's tiles
+      // stay in registers until every warp is done reading F, then P replaces it in the shared buffer
+      {
+        constexpr int NT5 = (NXB * NXB + TW - 1) / TW;
+        double acc[NT5][2];
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const int col = 4 * kk + fc;
-            double a = sF[fa + 16 * kk], bv = sF[fb + 16 * kk];
-            if (kb == i && col > fr) a = 0.0;
-            if (kb == j && col > fr) bv = 0.0;
-            dmma(acc, a, bv);
+        for (int q = 0; q < NT5; ++q) {
+          const int tile = tw + q * TW;
+          acc[q][0] = acc[q][1] = 0.0;
+          if (tile < NXB * NXB) {
+            const int i = tile / NXB, j = tile % NXB;
+            const int kbmax = i < j ? i : j;
+            for (int kb = 0; kb <= kbmax; ++kb) {
+              const int fa = tri_frag(t, 1 + i, 0, lane) + 32 * (1 + kb), fb = tri_frag(t, 1 + j, 0, lane) + 32 * (1 + kb);
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                const int col = 4 * kk + fc;
+                double a = sF[fa + 16 * kk], bv = sF[fb + 16 * kk];
+                if (kb == i && col > fr) a = 0.0;
+                if (kb == j && col > fr) bv = 0.0;
+                dmma(acc[q], a, bv);
+              }
+            }
           }
         }
+        team_sync(bar, tthreads);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) sP[full_off(8 * i + fr, 8 * j + 2 * fc + e, NX)] = acc[e];
+        for (int q = 0; q < NT5; ++q) {
+          const int tile = tw + q * TW;
+          if (tile < NXB * NXB) {
+            const int i = tile / NXB, j = tile % NXB;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) sP[full_off(8 * i + fr, 8 * j + 2 * fc + e, NX)] = acc[q][e];
+          }
+        }
       }
       team_sync(bar, tthreads);
     }
@@ -255,15 +282,20 @@ template <int NXB, int TW>
 static cudaError_t launch_chain(const ChainArgs &g, cudaStream_t st) {
   using Cfg = ChainCfg<NXB, TW>;
   auto kern = chain_kernel<NXB, TW>;
-  const int teams = 128 / (32 * TW);
+  const int teams = 1, threads = 32 * TW;  // a CTA is one team (see the barrier note in the kernel)
   const size_t smem = sizeof(double) * Cfg::TEAM * teams;
   static LaunchCache cache;
-  const int occ = cache.occupancy((const void *)kern, 128, smem);
+  static bool carve = false;
+  if (!carve) {  // seven 31 KB problems per SM need the largest shared-memory carve-out
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
+  const int occ = cache.occupancy((const void *)kern, threads, smem);
   ix grid = (g.batch + teams - 1) / teams;
   const ix cap = (ix)num_sms() * occ;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 128, smem, st>>>(g);
+  kern<<<(unsigned)grid, threads, smem, st>>>(g);
   note_launch();
   return cudaGetLastError();
 }
