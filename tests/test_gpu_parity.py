@@ -868,7 +868,7 @@ def test_riccati_chain_fused_kernel_vs_oracle():
     chain and the per-stage batched path."""
     from chain_util import make_problems, oracle_chain, packed_inputs
     from paper_1704_02457_b200.chain import RiccatiChain
-    for nb, nx, nu, N in [(16, 32, 8, 50), (7, 16, 8, 9), (5, 64, 8, 3)]:
+    for nb, nx, nu, N in [(16, 32, 8, 50), (7, 16, 8, 9), (5, 64, 8, 3), (9, 8, 8, 5), (6, 24, 8, 4), (4, 48, 8, 3)]:
         A, B, Q, R = make_problems(nb, nx, nu, seed=nx)
         BAt, RQ, P0 = packed_inputs(A, B, Q, R)
         ch = RiccatiChain(nb, nx, nu)
