@@ -424,7 +424,10 @@ __global__ void __launch_bounds__(256) trsm_team_kernel(TrsmArgs g, int team_ele
   const int team = warp / TW, tw = warp % TW;
   const int teams_per_cta = (blockDim.x >> 5) / TW;
   const int tthreads = TW * 32, ttid = tw * 32 + lane;
-  const int bar = 1 + team;
+  // one team per CTA (launch_trsm): the team barrier is the CTA barrier -- a runtime named-barrier id would
+  // reserve all 16 hardware barriers and cap the SM at 4 CTAs
+  auto team_sync = [&](int, int) { __syncthreads(); };
+  const int bar = 0;
   const int m = (int)g.m, n = (int)g.n;
   Tri t;
   t.cn8 = (n + 7) / 8 * 8;
@@ -610,10 +613,14 @@ static cudaError_t launch_trsm(const TrsmArgs &g, cudaStream_t st) {
   const ix cn8 = (g.n + 7) / 8 * 8;
   ix team_elems = Tri::size(g.n, g.n) + cn8 + 8 + 64 * (cn8 / 8) + (ix)TW * 8 * cn8;
   team_elems = (team_elems + 15) / 16 * 16;
-  int threads;
-  size_t smem;
-  const int teams = pick_teams(TW, team_elems, threads, smem);
+  const int teams = 1, threads = TW * 32;  // a CTA is one team (see the barrier note in the kernel)
+  const size_t smem = (size_t)team_elems * sizeof(double);
   static LaunchCache cache;
+  static bool carve = false;
+  if (!carve) {  // small triangles: many CTAs per SM want the largest shared-memory carve-out
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   const int occ = cache.occupancy((const void *)kern, threads, smem);
   ix grid = (g.batch + teams - 1) / teams;
   const ix cap = (ix)num_sms() * occ;
