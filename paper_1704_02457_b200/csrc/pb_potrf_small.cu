@@ -21,6 +21,8 @@
 // in-tile updates, IEEE sqrt and division, no FMA contraction -- so the
 // factor and diag_inv are bit-identical to the reference's.  Failure
 // index and the partially written factor of a failing item match too.
+#include <type_traits>
+
 #include "pb_gemm.cuh"
 
 namespace pb {
@@ -480,10 +482,44 @@ __global__ void __launch_bounds__(NTH, MINB) potrf_small1_kernel(PotrfArgs g) {
   const double *Cb = g.C.p;
   double *Db = g.D.p;
   const bool inplace = g.C.p == g.D.p && g.C.stride == g.D.stride && g.C.cn == g.D.cn && g.ci == g.di && g.cj == g.dj;
+  // Regular rounds (N = 4, 8: every panel's 16-byte piece count divides the CTA, the round is full, no item
+  // failed): a thread's piece (column, half) is the same in every trip and only the item advances, so the
+  // staging and store loops are one address + pointer increments instead of a division and two 64-bit
+  // products per piece (the n = 8 kernel spent a third of its instructions on that index math).
+  constexpr bool REGP = NP <= 2 && NTH % (2 * Cfg::cols(0)) == 0 && NTH % (2 * Cfg::cols(NP - 1)) == 0 && NTH % N == 0;
+  auto stage_panel = [&](auto pc, double *S, ix b0) {
+    constexpr int P = decltype(pc)::value, pieces = 2 * Cfg::cols(P), step = NTH / pieces;
+    const int it0 = tid / pieces, w = tid % pieces;
+    const double *src = Cb + (b0 + it0) * g.C.stride + eo(g.ci + 4 * P, g.cj + (w >> 1), g.C.cn) + 2 * (w & 1);
+    double *dst = S + it0 * STRIDE + Cfg::poff(P) + 2 * w;
+#pragma unroll
+    for (int k = 0; k < ITEMS / step; ++k) {
+      cp_async16(dst, src, 16);
+      src += (ix)step * g.C.stride;
+      dst += step * STRIDE;
+    }
+  };
+  auto store_panel = [&](auto pc, const double *S, ix b0) {
+    constexpr int P = decltype(pc)::value, pieces = 2 * Cfg::cols(P), step = NTH / pieces;
+    const int it0 = tid / pieces, w = tid % pieces;
+    const double *src = S + it0 * STRIDE + Cfg::poff(P) + 2 * w;
+    double *dst = Db + (b0 + it0) * g.D.stride + eo(g.di + 4 * P, g.dj + (w >> 1), g.D.cn) + 2 * (w & 1);
+#pragma unroll
+    for (int k = 0; k < ITEMS / step; ++k) {
+      *reinterpret_cast<double2 *>(dst) = *reinterpret_cast<const double2 *>(src);
+      src += step * STRIDE;
+      dst += (ix)step * g.D.stride;
+    }
+  };
 
   auto issue = [&](ix rd, int buf) {
     double *S = smem + buf * Cfg::BUF;
     const ix b0 = rd * ITEMS;
+    if (REGP && b0 + ITEMS <= g.batch) {
+      stage_panel(std::integral_constant<int, 0>{}, S, b0);
+      if constexpr (NP > 1) stage_panel(std::integral_constant<int, NP - 1>{}, S, b0);
+      return;
+    }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const int pieces = 2 * Cfg::cols(p);
@@ -567,7 +603,22 @@ __global__ void __launch_bounds__(NTH, MINB) potrf_small1_kernel(PotrfArgs g) {
           if (c < Cfg::cols(p) && WC::wr(p, c, r)) Si[Cfg::poff(p) + 4 * c + r] = L[4 * p + r][c];
     sinfo[it] = fail;
     if (bi < g.batch && g.info) g.info[bi] = fail;
-    __syncthreads();
+    const int anyfail = __syncthreads_or(fail >= 0);
+    if (REGP && !anyfail && b0 + ITEMS <= g.batch) {
+      // regular round: whole pieces, pointer increments only
+      store_panel(std::integral_constant<int, 0>{}, S, b0);
+      if constexpr (NP > 1) store_panel(std::integral_constant<int, NP - 1>{}, S, b0);
+      const double *ds = sdinv + tid;
+      double *dd = g.D.d + (b0 + tid / N) * g.D.dstride + g.dj + tid % N;
+#pragma unroll
+      for (int k = 0; k < ITEMS * N / NTH; ++k) {
+        *dd = *ds;
+        ds += NTH;
+        dd += (ix)(NTH / N) * g.D.dstride;
+      }
+      if (STG == 1) __syncthreads();
+      continue;
+    }
     // stores: every 16-byte piece of the lower prefix, whole, unless the
     // item failed (then exactly the reference's partial write set)
 #pragma unroll
