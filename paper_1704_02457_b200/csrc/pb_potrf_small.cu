@@ -736,7 +736,14 @@ cudaError_t run_potrf_small(const PotrfArgs &g, cudaStream_t st) {
     case 5: return launch_small1<5>(g, st);
     case 6: return launch_small1<6>(g, st);
     case 7: return launch_small1<7>(g, st);
-    case 8: return launch_small1<8>(g, st);
+    case 8: {
+      // single stage: with the regular-round staging / store loops the second stage only costs shared memory
+      // (config sweep, C2 n = 8 point, one box: <128,2,1> 19.30 ms, <128,1,3> 18.53, <64,2,4> 18.79,
+      // <128,1,2> 17.41 = 0.574 of HBM; in place <128,2,1> 0.67, <128,1,2> 0.66, <64,1,4> 0.72)
+      const bool ip = g.C.p == g.D.p && g.C.stride == g.D.stride && g.ci == g.di && g.cj == g.dj;
+      if (ip) return launch_small1<8, 64, 1, 4>(g, st);
+      return launch_small1<8, 128, 1, 2>(g, st);
+    }
 #define PB_SMALL(N_) \
   case N_:           \
     return launch_small_default<N_>(g, st);
