@@ -238,7 +238,7 @@ __device__ __forceinline__ int factor_t4s(double *Si, double *dinv, int q, volat
   return fail;
 }
 
-template <int N, int NTH_, int STAGES_, bool QRMW = false, int MINB = 1>
+template <int N, int NTH_, int STAGES_, bool QRMW = false, int MINB = 1, bool HOIST = false>
 __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
   constexpr int STG = Cfg::STAGES;
@@ -253,9 +253,33 @@ __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
 
   // stage the lower prefix of round `rd`'s items into buffer `buf`: panel p
   // of an item contributes columns [0, cols(p)) = 2*cols(p) 16-byte pieces
+  // Regular rounds of the quad path (HOIST; N % 4 == 0, full round, no failing item): a panel's prefix is
+  // walked in groups of four columns = eight 16-byte pieces, so a thread keeps ONE piece position
+  // (tid % 8) and item lane (tid / 8) for the whole round; every address is a base plus compile-time
+  // offsets and per-trip item strides -- no per-piece division, no 64-bit products.  It costs registers:
+  // at the 128-register cap of 8 CTAs/SM it spills (11.3 -> 12.4 ms at the C2 n = 16 point), at 6 CTAs/SM
+  // it does not (10.6 ms); in place the plain loops at 8 CTAs/SM stay ahead (10.7 vs 10.9 ms).
+  constexpr int GSTEP = NTH / 8;  // items covered by one trip of a column group
+  constexpr bool REGQ = HOIST && T == 4 && !QRMW && N % 4 == 0 && NTH % 8 == 0 && ITEMS % GSTEP == 0 &&
+                        NTH % N == 0 && (ITEMS * N) % NTH == 0;
+  const int gw = tid & 7, git = tid >> 3;
   auto issue = [&](ix rd, int buf) {
     double *S = smem + buf * Cfg::BUF;
     const ix b0 = rd * ITEMS;
+    if (REGQ && b0 + ITEMS <= g.batch && (g.ci & 3) == 0) {
+      const double *src0 = Cb + (b0 + git) * g.C.stride + g.ci * g.C.cn + 4 * g.cj + 2 * gw;
+      double *dst0 = S + git * STRIDE + 2 * gw;
+#pragma unroll
+      for (int k = 0; k < ITEMS / GSTEP; ++k) {
+        const double *src = src0 + (ix)k * GSTEP * g.C.stride;
+        double *dst = dst0 + k * GSTEP * STRIDE;
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+#pragma unroll
+          for (int cg = 0; cg <= p; ++cg) cp_async16(dst + Cfg::poff(p) + 16 * cg, src + (ix)4 * p * g.C.cn + 16 * cg, 16);
+      }
+      return;
+    }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       constexpr int dummy = 0;
@@ -360,7 +384,41 @@ __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
       if (b0 + it < g.batch && g.info) g.info[b0 + it] = fail;
     }
     if constexpr (RMW) cp_async_wait<1>();  // this thread's D pieces have landed
-    __syncthreads();
+    const int anyfail = __syncthreads_or(fail >= 0);
+    if (REGQ && !anyfail && b0 + ITEMS <= g.batch && (g.di & 3) == 0) {
+      const int cl = gw >> 1, h2 = 2 * (gw & 1);
+      const bool m0 = h2 >= cl, m1 = h2 + 1 >= cl;
+      const double *src0 = S + git * STRIDE + 2 * gw;
+      double *dst0 = Db + (b0 + git) * g.D.stride + g.di * g.D.cn + 4 * g.dj + 2 * gw;
+#pragma unroll
+      for (int k = 0; k < ITEMS / GSTEP; ++k) {
+        const double *src = src0 + k * GSTEP * STRIDE;
+        double *dst = dst0 + (ix)k * GSTEP * g.D.stride;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+#pragma unroll
+          for (int cg = 0; cg < p; ++cg)
+            *reinterpret_cast<double2 *>(dst + (ix)4 * p * g.D.cn + 16 * cg) =
+                *reinterpret_cast<const double2 *>(src + Cfg::poff(p) + 16 * cg);
+          const double2 v = *reinterpret_cast<const double2 *>(src + Cfg::poff(p) + 16 * p);
+          double *dd = dst + (ix)4 * p * g.D.cn + 16 * p;
+          if (m0) *reinterpret_cast<double2 *>(dd) = v;
+          else if (m1) dd[1] = v.y;
+        }
+      }
+      {
+        const double *ds = sdinv + tid;
+        double *dd = g.D.d + (b0 + tid / N) * g.D.dstride + g.dj + tid % N;
+#pragma unroll
+        for (int k = 0; k < ITEMS * N / NTH; ++k) {
+          *dd = *ds;
+          ds += NTH;
+          dd += (ix)(NTH / N) * g.D.dstride;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     // Stores of the reference's write set (lower triangle; on failure only
     // what the reference stored before returning).  Columns left of a
     // panel's diagonal block are entirely lower: full 16-byte pieces.  The
@@ -684,10 +742,10 @@ static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 1>
+template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 1, bool HOIST = false>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
-  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB>;
+  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB, HOIST>;
   static LaunchCache cache;
   const int occ = cache.occupancy((const void *)kern, Cfg::NTHREADS, Cfg::SMEM);
   const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
@@ -705,7 +763,13 @@ static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
 // best (n = 16: 13.84 -> 11.46 ms, profiles/r01_potrf_small_rmw.txt).
 template <int N>
 static cudaError_t launch_small_default(const PotrfArgs &g, cudaStream_t st) {
-  if constexpr (SmallCfg<N>::T == 4) return launch_small<N, 64, 1, false, 8>(g, st);
+  if constexpr (SmallCfg<N>::T == 4) {
+    if constexpr (N % 4 == 0) {
+      const bool ip = g.C.p == g.D.p && g.C.stride == g.D.stride && g.ci == g.di && g.cj == g.dj;
+      if (!ip) return launch_small<N, 64, 1, false, 6, true>(g, st);  // hoisted staging / store loops, 6 CTAs/SM
+    }
+    return launch_small<N, 64, 1, false, 8>(g, st);
+  }
   else return launch_small<N>(g, st);
 }
 
