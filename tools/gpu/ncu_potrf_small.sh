@@ -9,5 +9,5 @@ ncu --set full --clock-control none --import-source on -k regex:"potrf_small" -s
 ncu --set full --clock-control none --import-source on -k regex:"potrf_small" -s 3 -c 1 -o gpurun_out/prof_n16 \
   $CMD "potrf_l n=16" > gpurun_out/ncu_n16.log 2>&1; echo ncu16_rc=$?
 python bench.py --steps 1 --warmup 3 --no-cpu --no-gemm --no-e2e --no-inplace > gpurun_out/plain_c2.json 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -s 180 -c 400 --csv --log-file gpurun_out/launches_c2.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -s 180 -c 400 --csv --log-file gpurun_out/launches_c2_all.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu --no-gemm --no-e2e --no-inplace > gpurun_out/ncu_launch.log 2>&1; echo launch_rc=$?
