@@ -800,6 +800,110 @@ __global__ void __launch_bounds__(128, MINB) gemm_item_reg_kernel(GemmArgs g) {
   }
 }
 
+// gemm_nt, m = n = k = 4 exactly, one-panel windows (the C3 sweep's first point: 128-byte items, pure HBM
+// streaming).  The thread-per-item register kernel reads each item with eight 16-byte loads at a 128-byte
+// lane stride and reached 0.68 of HBM.  Here a CTA stages a round of 128 items cooperatively -- thread t
+// keeps ONE piece position (t % 8) and item lane (t / 8), so consecutive lanes move consecutive 16-byte
+// pieces (coalesced both ways) and every address is a base plus a per-trip item stride -- then each thread
+// multiplies its own item out of its (conflict-free, 18-double) shared-memory slot and leaves D there for
+// the coalesced store.  Same _store_block rules (alpha = 0 never reads A / B, beta = 0 never reads C).
+template <int NTH>
+__global__ void __launch_bounds__(NTH) gemm4_staged_kernel(GemmArgs g) {
+  constexpr int ITEMS = NTH, STR = 18, STEP = NTH / 8, TRIPS = ITEMS / STEP;
+  extern __shared__ __align__(16) double sm4[];
+  double *sA = sm4, *sB = sA + ITEMS * STR, *sC = sB + ITEMS * STR;
+  const int tid = threadIdx.x, w = tid & 7, it0 = tid >> 3;
+  const bool ab = g.alpha != 0.0, rc = g.beta != 0.0;
+  const ix offA = eo(g.ai, g.aj, g.A.cn) + 2 * w, offB = eo(g.bi, g.bj, g.B.cn) + 2 * w;
+  const ix offC = eo(g.ci, g.cj, g.C.cn) + 2 * w, offD = eo(g.di, g.dj, g.D.cn) + 2 * w;
+  const ix nrounds = (g.batch + ITEMS - 1) / ITEMS;
+  for (ix rd = blockIdx.x; rd < nrounds; rd += gridDim.x) {
+    const ix b0 = rd * ITEMS;
+    {
+      const double *pa = g.A.p + (b0 + it0) * g.A.stride + offA, *pb_ = g.B.p + (b0 + it0) * g.B.stride + offB;
+      const double *pc = g.C.p + (b0 + it0) * g.C.stride + offC;
+      const int so = it0 * STR + 2 * w;
+#pragma unroll
+      for (int k = 0; k < TRIPS; ++k) {
+        const bool ok = b0 + it0 + k * STEP < g.batch;
+        if (ab) {
+          cp_async16(sA + so + k * STEP * STR, ok ? pa + (ix)k * STEP * g.A.stride : g.A.p, ok ? 16 : 0);
+          cp_async16(sB + so + k * STEP * STR, ok ? pb_ + (ix)k * STEP * g.B.stride : g.B.p, ok ? 16 : 0);
+        }
+        if (rc) cp_async16(sC + so + k * STEP * STR, ok ? pc + (ix)k * STEP * g.C.stride : g.C.p, ok ? 16 : 0);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    {
+      // this thread's item: column l of A / B at slot + 4 l (rows 0..3 contiguous)
+      double *mA = sA + tid * STR;
+      const double *mB = sB + tid * STR, *mC = sC + tid * STR;
+      double acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      if (ab) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          const double2 a01 = *reinterpret_cast<const double2 *>(mA + 4 * l), a23 = *reinterpret_cast<const double2 *>(mA + 4 * l + 2);
+          const double2 b01 = *reinterpret_cast<const double2 *>(mB + 4 * l), b23 = *reinterpret_cast<const double2 *>(mB + 4 * l + 2);
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double2 c01 = make_double2(0.0, 0.0), c23 = c01;
+        if (rc) c01 = *reinterpret_cast<const double2 *>(mC + 4 * j), c23 = *reinterpret_cast<const double2 *>(mC + 4 * j + 2);
+        const double cv[4] = {c01.x, c01.y, c23.x, c23.y};
+        double v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = store_rule(g.alpha, acc[i][j], g.beta, cv[i]);
+        *reinterpret_cast<double2 *>(mA + 4 * j) = make_double2(v[0], v[1]);
+        *reinterpret_cast<double2 *>(mA + 4 * j + 2) = make_double2(v[2], v[3]);
+      }
+    }
+    __syncthreads();
+    {
+      double *pd = g.D.p + (b0 + it0) * g.D.stride + offD;
+      const int so = it0 * STR + 2 * w;
+#pragma unroll
+      for (int k = 0; k < TRIPS; ++k) {
+        const ix b = b0 + it0 + k * STEP;
+        if (b < g.batch && !(g.skip && g.skip[b] >= 0))
+          *reinterpret_cast<double2 *>(pd + (ix)k * STEP * g.D.stride) = *reinterpret_cast<const double2 *>(sA + so + k * STEP * STR);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static cudaError_t launch_gemm4_staged(const GemmArgs &g, cudaStream_t st) {
+  constexpr int NTH = 128;
+  auto kern = gemm4_staged_kernel<NTH>;
+  const size_t smem = sizeof(double) * NTH * 18 * (g.beta != 0.0 ? 3 : 2);
+  static LaunchCache cache;
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
+  const int occ = cache.occupancy((const void *)kern, NTH, smem);
+  const ix rounds = (g.batch + NTH - 1) / NTH;
+  ix grid = (ix)num_sms() * occ;
+  if (grid > rounds) grid = rounds;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, NTH, smem, st>>>(g);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <bool SYRK, int MINB = 1>
 static cudaError_t launch_item_reg(const GemmArgs &g, cudaStream_t st) {
   auto kern = gemm_item_reg_kernel<SYRK, MINB>;
@@ -909,6 +1013,10 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
     // (k <= 4 only: the per-thread staging of larger k does not fit shared memory)
     // register-direct kernel (C3 n = 4: 3.40 -> 3.01 ms over the staged one;
     // capping it at 4-6 CTAs/SM spills and is slower)
+    // the full 4 x 4 x 4 product (the C3 sweep's first point): cooperative staging, coalesced both ways
+    if (!SYRK && g.m == 4 && g.n == 4 && g.k == 4 && (g.A.stride & 1) == 0 && (g.B.stride & 1) == 0 &&
+        (g.C.stride & 1) == 0)
+      return launch_gemm4_staged(g, st);
     if (g.k <= 4) return launch_item_reg<SYRK>(g, st);
   }
   if (big <= 24) return dispatch_direct<SYRK>(g, st);

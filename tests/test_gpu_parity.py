@@ -497,8 +497,8 @@ def test_trsm_zero_pivot_leaves_item_untouched():
 
 def test_gemm_special_cases_exact():
     rng = np.random.default_rng(5)
-    for (m, n, k) in [(3, 5, 7), (8, 2, 7), (40, 40, 40), (70, 66, 9)]:
-        nb = 4
+    for (m, n, k) in [(3, 5, 7), (8, 2, 7), (40, 40, 40), (70, 66, 9), (4, 4, 4)]:  # 4x4x4: the staged kernel
+        nb = 4 if m != 4 else 300  # more than one 128-item round, ragged last round
         c = rng.uniform(-1, 1, (nb, m, n))
         dC = pack.panel_from_array(c)
         nanA = pack.panel_from_array(np.full((nb, m, k), np.nan))
@@ -519,6 +519,39 @@ def test_gemm_special_cases_exact():
         level3.gemm_nt(0, n, k, 1.0, a, b, 0.0, dC, dD)  # m=0 / n=0: no-op
         level3.gemm_nt(m, 0, k, 1.0, a, b, 0.0, dC, dD)
         assert torch.equal(before, dD.storage)
+
+
+def test_gemm4_staged_inplace_broadcast_and_window():
+    """m = n = k = 4 (cooperatively staged kernel): D == C in place, a broadcast B (stride 0), column-offset
+    windows and several rounds with a ragged tail, against the oracle item by item."""
+    rng = np.random.default_rng(44)
+    nb = 389
+    A = rand_batch(rng, nb, 4, 9)
+    B = rand_batch(rng, 1, 4, 6)
+    C = rand_batch(rng, nb, 8, 7)
+    dA, dB, dC = dev(A), dev(B), dev(C)
+    want = C.storage.copy()
+    for b in range(nb):
+        a = A.window(0, 5, 4, 4)[b]
+        bm = B.window(0, 2, 4, 4)[0]
+        c = C.window(4, 3, 4, 4)[b]
+        res = np.zeros((4, 4))
+        for i in range(4):
+            for j in range(4):
+                acc = 0.0
+                for l in range(4):
+                    acc = np.float64(a[i, l]) * bm[j, l] + acc
+                res[i, j] = 0.75 * acc + (-0.5) * c[i, j]
+        for i in range(4):
+            for j in range(4):
+                want[b, O.element_offset(4 + i, 3 + j, C.cn)] = res[i, j]
+    level3.gemm_nt(4, 4, 4, 0.75, dA.ref(0, 5), dB.ref(0, 2), -0.5, dC.ref(4, 3), dC.ref(4, 3))
+    got = host(dC)
+    mask = np.zeros(C.per, dtype=bool)
+    for i in range(4):
+        for j in range(4):
+            mask[O.element_offset(4 + i, 3 + j, C.cn)] = True
+    compare_storage(got, want, mask, 4, "gemm4 staged in place")
 
 
 def test_aliasing_and_determinism_bit_exact():
