@@ -90,16 +90,31 @@ enum { BOP_NT = 0, BOP_NN = 1, BOP_TRI = 2 };
 // straight from global memory.  Used for tiny items (one tile per item)
 // and as the any-alignment fallback of the NN modes.
 
-template <int MT, int NT, bool SYRK, int BOP = BOP_NT, int MINB = 1>
+// ONE: the tile is the whole item (every window the tiny-item dispatch sends here): unit = item, and the
+// per-lane fragment / accumulator offsets are hoisted out of the unit loop (no 64-bit divisions, no eo()
+// products per fragment -- ~300 -> ~80 instructions per 8 x 8 x 8 item).
+template <int MT, int NT, bool SYRK, int BOP = BOP_NT, int MINB = 1, bool ONE = false>
 __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix tiles_m, ix tiles_n, ix nunits) {
   const int lane = threadIdx.x & 31;
   const ix warp = (ix)blockIdx.x * (blockDim.x >> 5) + warp_uniform();
   const ix nwarps = (ix)gridDim.x * (blockDim.x >> 5);
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / k-col
   const ix ncols = SYRK ? g.m : g.n;
+  ix hA[MT], hB[NT], hC[MT], hD[MT];
+  if constexpr (ONE) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      hA[i] = eo(g.ai + 8 * i + fr, g.aj + fc, g.A.cn);
+      hC[i] = eo(g.ci + 8 * i + fr, g.cj + 2 * fc, g.C.cn);
+      hD[i] = eo(g.di + 8 * i + fr, g.dj + 2 * fc, g.D.cn);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) hB[j] = eo(g.bi + 8 * j + fr, g.bj + fc, g.B.cn);
+  }
   for (ix u = warp; u < nunits; u += nwarps) {
     ix b, tm, tn;
-    unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
+    if constexpr (ONE) b = u, tm = 0, tn = 0;
+    else unit_coords(u, tiles_m, tiles_n, SYRK, b, tm, tn);
     if (g.skip && g.skip[b] >= 0) continue;
     const ix rbase = tm * (8 * MT), cbase = tn * (8 * NT);
     const double *A = g.A.item(b);
@@ -118,7 +133,7 @@ __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix t
           cv[i][j][e] = 0.0;
           const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
           if (BOP != BOP_TRI && g.beta != 0.0 && in_store<SYRK>(r, c, g.m, g.n))
-            cv[i][j][e] = C[eo(g.ci + r, g.cj + c, g.C.cn)];
+            cv[i][j][e] = ONE ? C[hC[i] + 4 * (8 * j + e)] : C[eo(g.ci + r, g.cj + c, g.C.cn)];
         }
     if (g.alpha != 0.0 || BOP == BOP_TRI) {
       // triangular B: rows above this tile's first column are all zero
@@ -137,13 +152,13 @@ __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix t
 #pragma unroll
           for (int i = 0; i < MT; ++i) {
             const ix r = rbase + 8 * i + fr;
-            a[u][i] = (r < g.m && l < g.k) ? ldg_nc(A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
+            a[u][i] = (r < g.m && l < g.k) ? ldg_nc(ONE ? A + hA[i] + 4 * (l - fc) : A + eo(g.ai + r, g.aj + l, g.A.cn)) : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const ix r = cbase + 8 * j + fr;
             if (BOP == BOP_NT)
-              bb[u][j] = (r < ncols && l < g.k) ? ldg_nc(B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
+              bb[u][j] = (r < ncols && l < g.k) ? ldg_nc(ONE ? B + hB[j] + 4 * (l - fc) : B + eo(g.bi + r, g.bj + l, g.B.cn)) : 0.0;
             else
               bb[u][j] = (r < ncols && l < g.k && (BOP != BOP_TRI || l >= r))
                              ? ldg_nc(B + eo(g.bi + l, g.bj + r, g.B.cn))
@@ -170,7 +185,7 @@ __global__ void __launch_bounds__(256, MINB) gemm_direct_kernel(GemmArgs g, ix t
         for (int e = 0; e < 2; ++e) {
           const ix r = rbase + 8 * i + fr, c = cbase + 8 * j + 2 * fc + e;
           if (in_store<SYRK>(r, c, g.m, g.n))
-            D[eo(g.di + r, g.dj + c, g.D.cn)] = BOP == BOP_TRI ? __dmul_rn(g.alpha, acc[i][j][e])
+            D[ONE ? hD[i] + 4 * (8 * j + e) : eo(g.di + r, g.dj + c, g.D.cn)] = BOP == BOP_TRI ? __dmul_rn(g.alpha, acc[i][j][e])
                                                                : epilogue_value<SYRK>(g, r, c, acc[i][j][e], cv[i][j][e]);
         }
   }
@@ -948,7 +963,19 @@ static cudaError_t launch_direct(const GemmArgs &g, cudaStream_t st) {
   const ix cap = (ix)num_sms() * 8 * 8;  // ~8 resident CTAs of 8 warps per SM, a few waves
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  // min 3 CTAs/SM (<= 85 registers): C3 n = 8..24 6.25 -> 4.63 ms summed (n = 16 alone 9 % slower)
+  // min 3 CTAs/SM (<= 85 registers): C3 n = 8..24 6.25 -> 4.63 ms summed (n = 16 alone 9 % slower).
+  // One-tile items (m, n <= 8) are latency-bound, not register-bound: 8 CTAs/SM (32 registers, 64 resident
+  // warps) took C3 n = 8 from 22.4 to 16.5 ms (0.71 -> 0.97 of HBM); 2x2 tiles lose at anything above 3
+  // (n = 12: 14.2 / 15.1 / 21.0 ms at 3 / 4 / 5).  The hoisted one-tile-per-item path (ONE) pays for items of
+  // up to 2x2 tiles (n = 12 15.3 -> 14.1 ms) and costs spills at 3x3 (n = 20 9.0 -> 9.4 ms).
+  if constexpr (BOP == BOP_NT && MT * NT <= 4) {
+    if (per == 1) {
+      gemm_direct_kernel<MT, NT, SYRK, BOP, (MT * NT == 1 ? 8 : 3), true>
+          <<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   gemm_direct_kernel<MT, NT, SYRK, BOP, 3><<<(unsigned)blocks, threads, 0, st>>>(g, tiles_m, tiles_n, nunits);
   note_launch();
   return cudaGetLastError();
