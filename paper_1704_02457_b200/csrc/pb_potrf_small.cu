@@ -11,9 +11,11 @@
 //    the masked stores of the results are fully coalesced;
 //  * n <= 8: one thread owns one item, entirely in registers, and every
 //    touched 32-byte sector of D is stored whole (potrf_small1_kernel);
-//    9 <= n <= 16: a quad of threads owns one item, thread q owning panel q
-//    (rows 4q..4q+3), left-looking over 4-column blocks, computed in place
-//    in the staged shared-memory copy (block rows read back by broadcast).
+//    9 <= n <= 16: a quad of threads owns one item, lane q owning row q of
+//    every panel (row-cyclic: equal work per lane in every column block),
+//    left-looking over 4-column blocks, computed in place in the staged
+//    shared-memory copy (block rows read back by broadcast, the diagonal
+//    tile's pivots and multipliers exchanged by quad shuffles).
 //
 // Arithmetic follows the reference's per-element operation order exactly
 // (potrf_drv ccore.pyx:877-905, _kpotrf_core :404-438, _trsm_rltn_core
@@ -35,9 +37,13 @@ struct SmallCfg {
   static constexpr int STAGES = STAGES_;
   static constexpr int ITEMS = NTHREADS / T;
   __host__ __device__ static constexpr int cols(int p) { return 4 * p + 4 < N ? 4 * p + 4 : N; }
-  __host__ __device__ static constexpr int poff(int p) { return p == 0 ? 0 : poff(p - 1) + 4 * cols(p - 1); }
+  // doubles before panel p's prefix = 4 * sum of cols(j), j < p; closed form (a recursive definition is compiled
+  // as an out-of-line loop wherever p is not folded: 10 calls per n = 16 item in the plain staging / store loops)
+  __host__ __device__ static constexpr int poff(int p) { return p < NP ? 8 * p * (p + 1) : 8 * (NP - 1) * NP + 4 * N; }
   static constexpr int ITEM_ELEMS = poff(NP);        // lower-prefix doubles per item
-  static constexpr int STRIDE = ITEM_ELEMS + 2;      // padded (16-byte aligned, odd 16-byte units)
+  // padded item stride, 16-byte aligned: thread-per-item reads 16-byte pieces at the item stride (odd
+  // 16-byte units); the quad path reads 8 bytes per lane = 32 contiguous bytes per quad (odd 32-byte units)
+  static constexpr int STRIDE = T == 1 ? ITEM_ELEMS + 2 : ITEM_ELEMS + (20 - ITEM_ELEMS % 16) % 16;
   static constexpr int BUF = ITEMS * STRIDE;
   static constexpr int DINV = ITEMS * N;  // one round's reciprocals
   static constexpr size_t SMEM = sizeof(double) * (STAGES * BUF + DINV) + sizeof(int) * ITEMS;
@@ -131,107 +137,82 @@ __device__ __forceinline__ int factor_t1(double (&L)[4 * SmallCfg<N>::NP][N], do
   return -1;
 }
 
-// One item, a quad of threads (9 <= n <= 16), computed IN SHARED MEMORY:
-// thread q owns panel q (rows 4q..4q+3) of the staged lower prefix; the
-// block row s it downdates against is read back from shared memory
-// (broadcast), so no register copy of the item is needed (few registers,
-// many warps per SM).  Left-looking over 4-column blocks; per element the
-// reference's operation order, IEEE sqrt/div, no FMA: bit-identical.
+// One item, a quad of threads (9 <= n <= 16), computed IN SHARED MEMORY with
+// ROW-CYCLIC ownership: lane q of the quad owns row q of every panel (rows
+// q, 4 + q, 8 + q, 12 + q).  Left-looking over 4-column blocks: for block s
+// every lane downdates its rows of panels s..NP-1 against block row s (read
+// back from shared memory by broadcast), so all four lanes carry the same
+// amount of work in every block (a panel-per-lane split leaves lane 0 idle
+// after block 0 and lane 3 with 2.4x the mean downdate).  The 4x4 diagonal
+// tile has one row per lane: its pivot and the multipliers L[4s+c2][4s+c]
+// travel by quad shuffles, sqrt / reciprocal are computed by all four lanes
+// (lockstep, no second broadcast), and the rows below are solved in the same
+// right-looking sweep.  Per element the reference's operation order (downdate
+// sum from 0.0 over l ascending, + C, - L[r][t] * L[c][t] over t ascending,
+// * 1/ljj), IEEE sqrt/div, no FMA: bit-identical.  No branch depends on the
+// data: after a bad pivot the lanes keep computing on dead values and only
+// the stores are switched off (the shuffles stay warp-uniform).
 template <int N>
-__device__ __forceinline__ int factor_t4s(double *Si, double *dinv, int q, volatile int *flag) {
+__device__ __forceinline__ int factor_t4c(double *Si, double *dinv, int q) {
   using Cfg = SmallCfg<N>;
   constexpr int NP = Cfg::NP;
+  const int qb = (threadIdx.x & 31) & ~3;  // first lane of this quad
   int fail = -1;
-  const bool own = q < NP;
-  double *Lq = Si + (own ? Cfg::poff(q < NP ? q : 0) : 0);  // element (r, l) at Lq[4l + r]
-  if (q == 0) *flag = -1;
-  __syncwarp();
+  double *Sq = Si + q;  // element (4p + q, l) at Sq[poff(p) + 4l]
 #pragma unroll
   for (int s = 0; s < NP; ++s) {
     const int ns = N - 4 * s < 4 ? N - 4 * s : 4;
-    const double *Ls = Si + Cfg::poff(s);  // block row s: element (c, l) at Ls[4l + c]
-    const bool act = own && q >= s && fail < 0;
-    double acc[4][4];
+    const double *Ls = Si + Cfg::poff(s);  // block row s: element (4s + c, l) at Ls[4l + c]
+    double acc[NP][4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[c][r] = 0.0;
-    if (act) {
+      for (int c = 0; c < 4; ++c) acc[p][c] = 0.0;
 #pragma unroll
-      for (int l = 0; l < 4 * s; ++l) {
-        const double2 lo = *reinterpret_cast<const double2 *>(Lq + 4 * l);
-        const double2 hi = *reinterpret_cast<const double2 *>(Lq + 4 * l + 2);
-        const double lr[4] = {lo.x, lo.y, hi.x, hi.y};
+    for (int l = 0; l < 4 * s; ++l) {
+      const double2 lo = *reinterpret_cast<const double2 *>(Ls + 4 * l);
+      const double2 hi = *reinterpret_cast<const double2 *>(Ls + 4 * l + 2);
+      const double v[4] = {lo.x, lo.y, hi.x, hi.y};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < ns) {
-            const double v = Ls[4 * l + c];
+      for (int p = s; p < NP; ++p) {
+        const double x = Sq[Cfg::poff(p) + 4 * l];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) acc[c][r] = dadd(acc[c][r], dmul(lr[r], -v));
-          }
-        }
+        for (int c = 0; c < 4; ++c)
+          if (c < ns) acc[p][c] = dadd(acc[p][c], dmul(x, -v[c]));
       }
+    }
+#pragma unroll
+    for (int p = s; p < NP; ++p)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
+        if (c < ns) acc[p][c] = dadd(acc[p][c], Sq[Cfg::poff(p) + 4 * (4 * s + c)]);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (c < ns) acc[c][r] = dadd(acc[c][r], Lq[4 * (4 * s + c) + r]);
-    }
-    if (act && q == s) {
-      int f = -1;
+    for (int c = 0; c < 4; ++c) {
+      if (c < ns) {
+        const double d = __shfl_sync(0xffffffffu, acc[s][c], qb + c);  // pivot: row c of the tile
+        if (fail < 0 && d <= 0.0) fail = 4 * s + c;                    // ccore.pyx:423 (NaN passes)
+        const double ljj = __dsqrt_rn(d);
+        const double inv = __ddiv_rn(1.0, ljj);
+        if (fail < 0 && q == 0) dinv[4 * s + c] = inv;
+        acc[s][c] = q == c ? ljj : dmul(acc[s][c], inv);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < ns && f < 0) {
-          const double d = acc[c][c];
-          if (d <= 0.0) {
-            f = c;
-          } else {
-            const double ljj = __dsqrt_rn(d);
-            const double inv = __ddiv_rn(1.0, ljj);
-            acc[c][c] = ljj;
-            dinv[4 * s + c] = inv;
+        for (int p = s + 1; p < NP; ++p) acc[p][c] = dmul(acc[p][c], inv);
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-              if (r > c) acc[c][r] = dmul(acc[c][r], inv);
+        for (int c2 = c + 1; c2 < 4; ++c2) {
+          if (c2 < ns) {
+            const double lcj = __shfl_sync(0xffffffffu, acc[s][c], qb + c2);  // L[4s + c2][4s + c]
 #pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2)
-              if (c2 > c && c2 < ns) {
-                const double lcj = acc[c][c2];
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-                  if (r >= c2) acc[c2][r] = dsub(acc[c2][r], dmul(acc[c][r], lcj));
-              }
+            for (int p = s; p < NP; ++p) acc[p][c2] = dsub(acc[p][c2], dmul(acc[p][c], lcj));
           }
         }
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (c < ns && r >= c && (f < 0 || c < f)) Lq[4 * (4 * s + c) + r] = acc[c][r];
-      if (f >= 0) *flag = 4 * s + f;
     }
-    __syncwarp();
-    fail = *flag;
-    if (act && q > s && fail < 0) {
+    if (fail < 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < ns) {
+      for (int p = s; p < NP; ++p)
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (t < c) {
-              const double e = Ls[4 * (4 * s + t) + c];
-#pragma unroll
-              for (int r = 0; r < 4; ++r) acc[c][r] = dsub(acc[c][r], dmul(acc[t][r], e));
-            }
-          const double inv = dinv[4 * s + c];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            acc[c][r] = dmul(acc[c][r], inv);
-            Lq[4 * (4 * s + c) + r] = acc[c][r];
-          }
-        }
-      }
+        for (int c = 0; c < 4; ++c)
+          if (c < ns && 4 * p + q < N && (p > s || q >= c)) Sq[Cfg::poff(p) + 4 * (4 * s + c)] = acc[p][c];
     }
     __syncwarp();
   }
@@ -376,7 +357,7 @@ __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
             *reinterpret_cast<double2 *>(Si + Cfg::poff(p) + 4 * c + 2) = make_double2(L[4 * p + 2][c], L[4 * p + 3][c]);
           }
     } else {
-      fail = factor_t4s<N>(Si, di, q, (volatile int *)(sinfo + it));
+      fail = factor_t4c<N>(Si, di, q);
     }
     const ix b0 = rd * ITEMS;
     if (q == 0) {
@@ -757,16 +738,18 @@ static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Default shape.  The quad path (9 <= n <= 16) is latency bound (FP64
-// dependency chains, 2 warps per scheduler at 246 registers): single-stage
-// 64-thread CTAs capped at 128 registers put 16 warps on an SM and measured
-// best (n = 16: 13.84 -> 11.46 ms, profiles/r01_potrf_small_rmw.txt).
+// Default shape of the quad path (9 <= n <= 16), row-cyclic factor, C2 n = 16 point on one box
+// (profiles/r02_potrf_n16_rowcyclic.txt): D != C <64,1,6,hoisted> 7.63 ms = 0.589 of HBM (<64,2,4> and <32,2,8>
+// 8.9-9.0, plain loops <64,1,8> 9.19, <64,1,6> 9.59, two plain stages 9.8-10.1); in place <32,2,8,hoisted> 6.86 ms =
+// 0.655 (<64,2,4> 7.19, plain <64,1,8> 8.46).  The hoisted loops need n % 4 == 0 and NTH % n == 0, so n = 12 and
+// the ragged sizes run the plain loops at 6 / 8 CTAs per SM.
 template <int N>
 static cudaError_t launch_small_default(const PotrfArgs &g, cudaStream_t st) {
   if constexpr (SmallCfg<N>::T == 4) {
     if constexpr (N % 4 == 0) {
       const bool ip = g.C.p == g.D.p && g.C.stride == g.D.stride && g.ci == g.di && g.cj == g.dj;
       if (!ip) return launch_small<N, 64, 1, false, 6, true>(g, st);  // hoisted staging / store loops, 6 CTAs/SM
+      if constexpr (N == 16) return launch_small<N, 32, 2, false, 8, true>(g, st);
     }
     return launch_small<N, 64, 1, false, 8>(g, st);
   }
