@@ -219,7 +219,11 @@ __device__ __forceinline__ int factor_t4c(double *Si, double *dinv, int q) {
   return fail;
 }
 
-template <int N, int NTH_, int STAGES_, bool QRMW = false, int MINB = 1, bool HOIST = false>
+__device__ __forceinline__ void prefetch_l2_small(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int N, int NTH_, int STAGES_, bool QRMW = false, int MINB = 1, bool HOIST = false, bool PF = false>
 __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
   constexpr int STG = Cfg::STAGES;
@@ -309,6 +313,14 @@ __global__ void __launch_bounds__(NTH_, MINB) potrf_small_kernel(PotrfArgs g) {
       cp_async_wait<0>();
     }
     __syncthreads();
+    if constexpr (PF && STG == 1 && T == 4 && NP == 4) {
+      // single stage: pull the next round's panel prefixes into L2 while this round is factored
+      const ix rn = rd + gridDim.x;
+      const int it2 = tid / NP, pp = tid % NP;
+      const ix b = rn * ITEMS + it2;
+      if (rn < nrounds && b < g.batch && (g.ci & 3) == 0)
+        prefetch_l2_small(Cb + b * g.C.stride + eo(g.ci + 4 * pp, g.cj, g.C.cn), (unsigned)(Cfg::cols(pp) * 32));
+    }
     double *S = smem + buf * Cfg::BUF;
     const int it = tid / T, q = tid % T;
     double *Si = S + it * STRIDE;
@@ -723,10 +735,10 @@ static cudaError_t launch_small1(const PotrfArgs &g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 1, bool HOIST = false>
+template <int N, int NTH_ = 128, int STAGES_ = 2, bool QRMW = false, int MINB = 1, bool HOIST = false, bool PF = false>
 static cudaError_t launch_small(const PotrfArgs &g, cudaStream_t st) {
   using Cfg = SmallCfg<N, NTH_, STAGES_>;
-  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB, HOIST>;
+  auto kern = potrf_small_kernel<N, NTH_, STAGES_, QRMW, MINB, HOIST, PF>;
   static LaunchCache cache;
   const int occ = cache.occupancy((const void *)kern, Cfg::NTHREADS, Cfg::SMEM);
   const ix rounds = (g.batch + Cfg::ITEMS - 1) / Cfg::ITEMS;
@@ -748,7 +760,8 @@ static cudaError_t launch_small_default(const PotrfArgs &g, cudaStream_t st) {
   if constexpr (SmallCfg<N>::T == 4) {
     if constexpr (N % 4 == 0) {
       const bool ip = g.C.p == g.D.p && g.C.stride == g.D.stride && g.ci == g.di && g.cj == g.dj;
-      if (!ip) return launch_small<N, 64, 1, false, 6, true>(g, st);  // hoisted staging / store loops, 6 CTAs/SM
+      // hoisted staging / store loops, 6 CTAs/SM, L2 prefetch of the next round (n = 16: 7.54 -> 7.41 ms)
+      if (!ip) return launch_small<N, 64, 1, false, 6, true, true>(g, st);
       if constexpr (N == 16) return launch_small<N, 32, 2, false, 8, true>(g, st);
     }
     return launch_small<N, 64, 1, false, 8>(g, st);
