@@ -57,19 +57,29 @@ __device__ __forceinline__ double epilogue_value(const GemmArgs &g, ix r, ix c, 
   return store_rule(g.alpha, acc, g.beta, cv);
 }
 
+// unit -> (item, tile row, tile column).  Every warp of a CTA calls this once per unit, and a 64-bit division is an
+// out-of-line ~80-instruction routine (two of them were as many instructions as a warp's share of a 32 x 32 x 36
+// tile): one tile per item needs no division at all, and unit indices below 2^32 divide in 32 bits.
 __device__ __forceinline__ void unit_coords(ix u, ix tiles_m, ix tiles_n, bool syrk, ix &b, ix &tm, ix &tn) {
-  if (!syrk) {
-    const ix per = tiles_m * tiles_n;
-    b = u / per;
-    const ix t = u % per;
-    tm = t / tiles_n;
-    tn = t % tiles_n;
+  const ix per = syrk ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  if (per == 1) {
+    b = u, tm = 0, tn = 0;
+    return;
+  }
+  unsigned t;
+  if (((unsigned long long)u >> 32) == 0 && ((unsigned long long)per >> 32) == 0) {
+    const unsigned uu = (unsigned)u, pp = (unsigned)per, q = uu / pp;
+    b = q, t = uu - q * pp;
   } else {
-    const ix per = tiles_m * (tiles_m + 1) / 2;
     b = u / per;
-    ix t = u % per;
+    t = (unsigned)(u - b * per);  // tiles per item fit 32 bits (m, n < 2^31 / tile)
+  }
+  if (!syrk) {
+    const unsigned tnn = (unsigned)tiles_n, q = t / tnn;
+    tm = q, tn = t - q * tnn;
+  } else {
     // lower-triangular tile index -> (tm, tn), tn <= tm
-    ix r = (ix)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    unsigned r = (unsigned)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
     while (r * (r + 1) / 2 > t) --r;
     while ((r + 1) * (r + 2) / 2 <= t) ++r;
     tm = r;
