@@ -1074,7 +1074,9 @@ static cudaError_t dispatch_gemm(GemmArgs g, cudaStream_t st) {
     const double wcost[8] = {1.000, 1.081, 1.056, 1.241, 1.107, 1.422, 1.350, 1.182};
     for (int i = 0; i < 8; ++i) {
       const int t = tiles[i];
-      const double area = (double)((g.m + t - 1) / t * t) * (double)((ncols + t - 1) / t * t) * wcost[i];
+      const ix tmr = (g.m + t - 1) / t, tnc = (ncols + t - 1) / t;
+      // syrk runs the lower tiles only: tmr (tmr + 1) / 2 of them
+      const double area = (SYRK ? 0.5 * (double)(tmr * (tmr + 1)) : (double)(tmr * tnc)) * (double)t * (double)t * wcost[i];
       if (area < best * 0.999) best = area, T = t;
     }
     const bool k40 = g.k > 32 && g.k <= 40;
